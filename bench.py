@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the reduction hot path; prints ONE JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {b200,reference}]
+                    [--dtype float32] [--op sum] [--log2n 28]
+
+A "step" is one pass of the whole hot path (plus a8
+when N > 1) over the synthetic input resident in HBM: one `reduce` call (one
+kernel launch) at N = 1; one `reduce_multi` call (reduce kernel, NCCL
+all-gather of 32-byte records, rank-order combine kernel) at N > 1.
+
+Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
+float32 sum, n = 2^28 elements (1 GiB) per GPU, u01 data (inputs/, seed 1);
+at N > 1 rank r holds global indices [r*2^28, (r+1)*2^28) of one 2^28*N array
+(weak scaling). The input is 8x the 126 MB L2, so there is no L2 flush: each
+pass streams from HBM.
+
+`--impl reference` times the CPU oracle (oracle/, Algorithm 1 of PAPER.md
+P:27-40) as it stands on the host, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "reduce GB/s and % of HBM peak (fp32/int32, n=2^28..2^34) at 1/2/4/8 B200"
+NP_BYTES = {"int32": 4, "uint32": 4, "int64": 8, "float32": 4, "float64": 8}
+DTYPE_TAG = {"int32": "i32", "uint32": "u32", "int64": "i64", "float32": "f32", "float64": "f64"}
+
+
+def gbps(nbytes: float, seconds: float) -> float:
+    """Decimal GB/s, the paper's convention (Table 2: n*4 bytes / time)."""
+    return nbytes / seconds / 1e9
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: torch copy, read+write bytes)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload_key: str):
+    """Per-launch dram bytes of the reduce kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(workload_key)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return self
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self.thread:
+                self.thread.join(timeout=2)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        loaded = [r for r in self.rows if r[2].isdigit() and int(r[2]) > 0] or self.rows
+        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in loaded for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows), "samples_under_load": len(loaded)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ====================================================================== reference arm
+def run_reference(args):
+    """The oracle as it stands, on the host cores, on a bounded sample per step."""
+    import numpy as np
+    import inputs
+    import oracle
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    dt, op = args.dtype, args.op
+    s = NP_BYTES[dt]
+    n_full = 1 << args.log2n
+    # size the per-step sample so the whole run stays within ~2 minutes
+    probe = inputs.generate(1 << 20, dt, "u01" if dt.startswith("float") else inputs.default_workload(dt, op))
+    t0 = time.perf_counter()
+    oracle.reduce(probe, op)
+    rate = (1 << 20) / (time.perf_counter() - t0)      # elements / s
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    m = int(min(n_full, max(1 << 16, rate * budget)))
+    wl = "u01" if dt.startswith("float") else inputs.default_workload(dt, op)
+    x = inputs.generate(m, dt, wl, seed=1, offset=0, n_total=n_full)
+    for _ in range(args.warmup):
+        oracle.reduce(x, op)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.reduce(x, op)
+    dt_s = time.perf_counter() - t0
+    v = gbps(m * s * args.steps, dt_s)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt_s / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": DTYPE_TAG[dt], "data": "synthetic",
+        "config": {"workload": f"{dt} {op}, n=2^{args.log2n} per GPU (u01, seed 1); "
+                               f"each reference step folds the first {m} elements (bounded sample)",
+                   "n_per_gpu": n_full, "op": op, "sample_elements": m},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": f"first {m} of {n_full} elements per step, {args.steps} steps"},
+        "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ====================================================================== B200 arm
+def run_b200(args):
+    import numpy as np
+    import torch
+    import inputs
+    import paper_1710_07358_b200 as rd
+
+    ws, rank, local = dist_env()
+    if ws != args.gpus:
+        if args.gpus > 1:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    dt, op = args.dtype, args.op
+    s = NP_BYTES[dt]
+    n = 1 << args.log2n                              # per GPU (weak scaling)
+    wl = "u01" if dt.startswith("float") else inputs.default_workload(dt, op)
+    x = torch.empty(n, dtype=getattr(torch, dt), device=dev)
+    inputs.fill_device(x, wl, seed=1, offset=rank * n, n_total=n * ws)
+    out = torch.empty((), dtype=x.dtype, device=dev)
+    comm = rd.Comm.from_process_group() if ws > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if comm is None:
+            rd.reduce(x, op, out=out)
+        else:
+            comm.reduce(x, op, out=out)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # warm-up (also creates the per-stream workspace)
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local).start()
+    # clock soak: ~1 s of the same work so the clock record sees a loaded GPU
+    t_end = time.perf_counter() + (0.0 if args.profile else 1.0)
+    while time.perf_counter() < t_end:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize(dev)
+
+    # ---------------- timed region: exactly K steps
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    t0.record(stream)
+    for i in range(K):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    t1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    total_ms = t0.elapsed_time(t1)
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    if ws > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = gbps(n * s * ws * K, total_ms / 1e3)
+
+    # ---------------- dominant kernel (the reduce kernel) alone, for the roofline
+    if comm is None:
+        kern_ms = statistics.mean(step_ms)          # one launch per step
+        kern_src = "per-step CUDA events in the timed region (1 launch per step)"
+    else:
+        rec = torch.empty(32, dtype=torch.uint8, device=dev)
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        for i in range(K):
+            kev[i][0].record(stream)
+            rd.reduce_partial(x, op, rec=rec)
+            kev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+        kern_src = "CUDA events around the same reduce kernel (reduce_partial), K launches after the timed region"
+    peak, peak_src = load_peaks()
+    achieved = gbps(n * s, kern_ms / 1e3)
+
+    # check the timed result once (cheap property: finite, plausible)
+    res = out.item()
+
+    # ---------------- e2e: host (pinned) -> device -> result -> host, through the public API
+    ke = 0 if args.profile else max(3, min(K, 10))
+    host = torch.empty(n if ke else 0, dtype=x.dtype, pin_memory=True)
+    if ke:
+        host.copy_(x)
+    torch.cuda.synchronize(dev)
+    if ke == 0:
+        te, e2e_timer = float("nan"), "skipped (--profile)"
+    elif comm is None:
+        rd.reduce_host(host, op)                         # warm the pipeline
+        te = time.perf_counter()
+        for _ in range(ke):
+            rd.reduce_host(host, op)
+        te = time.perf_counter() - te
+        e2e_timer = "host perf_counter around synchronous reduce_host calls (chunked H2D overlapped with reduce)"
+    else:
+        barrier()
+        te = time.perf_counter()
+        for _ in range(ke):
+            x.copy_(host, non_blocking=True)
+            comm.reduce(x, op, out=out)
+            out.item()
+        te = time.perf_counter() - te
+        import torch.distributed as dist
+        tt = torch.tensor([te], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+        e2e_timer = "host perf_counter, max over ranks: pinned H2D copy + reduce_multi + .item() per step"
+    e2e = {"value": round(gbps(n * s * ws * ke, te), 3) if ke else None, "unit": "GB/s",
+           "h2d_bytes_per_step": n * s * ws, "d2h_bytes_per_step": s * ws,
+           "steps": ke, "timer": e2e_timer}
+
+    line = None
+    if rank == 0:
+        # ---------------- context: torch.sum on the same tensor (library reduction)
+        tctx = None
+        if op == "sum" and not args.profile:
+            for _ in range(3):
+                torch.sum(x)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(20):
+                torch.sum(x)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            tctx = round(gbps(n * s * 20, a.elapsed_time(b) / 1e3), 2)
+
+        # ---------------- cpu_baseline: the oracle on the host, rank 0, N = 1 only
+        cpu = None
+        if ws == 1 and not args.no_cpu and not args.profile:
+            import oracle
+            xh = host.numpy()
+            passes, tc = 0, time.perf_counter()
+            m = n
+            while True:
+                oracle.reduce(xh[:m], op)
+                passes += 1
+                el = time.perf_counter() - tc
+                if el > args.cpu_seconds or passes >= 50:
+                    break
+            cpu = {"value": round(gbps(m * s * passes, el), 4), "unit": "GB/s", "cores": 1,
+                   "kind": "oracle",
+                   "sample": f"{passes} full pass(es) over the same {n}-element host array "
+                             f"({el:.1f} s, single thread, gcc -O2)"}
+
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": K,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / K, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_TAG[dt], "data": "synthetic",
+            "config": {"workload": f"{dt} {op}, n=2^{args.log2n} per GPU ({wl}, seed 1), BASELINE configs[1]",
+                       "n_per_gpu": n, "n_total": n * ws, "op": op,
+                       "l2": "input (%.2f GB/GPU) > 126 MB L2: no flush" % (n * s / 1e9),
+                       "parallelism": f"shard{ws}" if ws > 1 else "single"},
+            "pct_hbm_peak": round(100 * value / (peak * ws), 2),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4),
+                         "traffic": load_traffic(f"{dt}-{op}-2^{args.log2n}"),
+                         "kernel_ms": round(kern_ms, 5), "peak_source": peak_src,
+                         "achieved_source": kern_src,
+                         "algorithmic_bytes_per_launch": n * s},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": K * (1 if comm is None else 2),
+            "clocks": clocks,
+            "context": {"torch_sum_gbs": tctx, "result": res},
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        comm.destroy()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--dtype", default="float32", choices=list(NP_BYTES))
+    p.add_argument("--op", default="sum")
+    p.add_argument("--log2n", type=int, default=28)
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--profile", action="store_true",
+                   help="for ncu: no clock soak, e2e, cpu baseline or context rows (not a bench value)")
+    args = p.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,193 @@
+/*
+ * b200reduce.h -- C ABI of the B200-native (sm_100a) reduction library.
+ *
+ * The operation (§1.1 "Problem Definition"):
+ *   "Given a set X with n values, X = {x_0, x_1, ..., x_{n-1}}, compute
+ *    x_0 (x) x_1 (x) ... (x) x_{n-1}. The associative operator (x) ... can be
+ *    (but is not limited to) any one of the set {+, x, AND, OR, XOR, ..., max, min}."
+ * evaluated in any order, which associativity and commutativity allow
+ * (P:42-50); the result for an empty X is the initial accumulator of
+ * Algorithm 1 "Summation(A)" (`accumulator <- 0`; INFINITY for min,
+ * Listing 1 ln041).
+ *
+ * The GPU structure follows the two-stage reduction with the
+ * paper's unrolled persistent-thread Step 1, re-designed for
+ * sm_100a: one single-pass launch whose grid-level combine ("Stage 2")
+ * is done by the last CTA to finish, through an atomic ticket.
+ *
+ * Conventions for every entry point
+ *  - All functions return rd_status; no C++ exception crosses the ABI.
+ *  - Arguments are validated synchronously BEFORE anything is enqueued; a call
+ *    that returns an error enqueued nothing and left every output untouched.
+ *  - Device entry points are asynchronous and stream-ordered on `stream`
+ *    (a cudaStream_t; NULL = the legacy default stream). They never
+ *    synchronise the host and are capturable in CUDA graphs once the
+ *    per-(device, stream) workspace exists (it is created by the first call
+ *    on that stream, outside capture).
+ *  - Element-aligned base pointers are required (x % sizeof(dtype) == 0,
+ *    else RD_ERR_MISALIGNED); any element offset is valid.
+ *  - Bitwise ops (AND/OR/XOR) on float dtypes -> RD_ERR_UNSUPPORTED.
+ *  - n == 0 writes the empty result (table below) and returns RD_OK.
+ *
+ * Results:
+ *  - integers: + and x wrap modulo 2^w; min/max signed for int32/int64,
+ *    unsigned for uint32; AND/OR/XOR on raw bits. Bit-exact for any order.
+ *  - float min/max: IEEE 754-2019 minimum/maximum (NaN propagates as a quiet
+ *    NaN, -0.0 < +0.0). Bit-exact.
+ *  - float +: fp32 accumulates in fp32, fp64 in fp64, in a fixed tree order;
+ *    |result - exact| <= 4 * eps(dtype) * sum|x_i| on the workloads of
+ *    DESIGN.md. A zero sum is -0.0 iff every x_i is -0.0; empty -> +0.0.
+ *  - float x: fp32 accumulates in fp64, fp64 in double-double, then one
+ *    rounding; |result - exact| <= 4 * eps(dtype) * |exact| when no partial
+ *    product over/underflows.
+ *  - Determinism: identical (x, n, base alignment, dtype, op, device) give
+ *    identical bits (no float atomics; every combine is in a fixed order).
+ *
+ *  empty results:   +   x    min          max          and   or  xor
+ *      int32        0   1    INT32_MAX    INT32_MIN    -1    0   0
+ *      uint32       0   1    UINT32_MAX   0            ~0u   0   0
+ *      int64        0   1    INT64_MAX    INT64_MIN    -1    0   0
+ *      float32/64  +0.0 1.0  +inf         -inf         (unsupported)
+ */
+#ifndef B200REDUCE_H
+#define B200REDUCE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { RD_INT32 = 0, RD_UINT32 = 1, RD_INT64 = 2, RD_FLOAT32 = 3, RD_FLOAT64 = 4 } rd_dtype;
+typedef enum { RD_SUM = 0, RD_PROD = 1, RD_MIN = 2, RD_MAX = 3, RD_AND = 4, RD_OR = 5, RD_XOR = 6 } rd_op;
+typedef enum {
+  RD_OK = 0,
+  RD_ERR_INVALID_ARG = 1,  /* NULL where a buffer is needed, unknown enum, bad config  */
+  RD_ERR_UNSUPPORTED = 2,  /* bitwise op on a float dtype                              */
+  RD_ERR_MISALIGNED = 3,   /* base pointer not aligned to sizeof(dtype)                */
+  RD_ERR_CUDA = 4,         /* CUDA launch / allocation / copy failure (rd_last_error)  */
+  RD_ERR_NCCL = 5,         /* NCCL failure (rd_last_error)                             */
+  RD_ERR_MISMATCH = 6      /* ranks or records disagree on dtype/op                    */
+} rd_status;
+
+/* A CUDA stream handle; identical to cudaStream_t / CUstream. */
+typedef struct CUstream_st* rd_stream_t;
+
+/*
+ * rd_record -- the un-narrowed partial result of one block of X.
+ * 32 bytes, plain data, device- or host-resident. Partials are what the
+ * two-stage structure passes between its stages (the |SM|-sized "result"
+ * vector of P:143/P:174); here they are what shards exchange.
+ *   tag    = 0x52440000 | dtype << 8 | op      (0 marks "no record")
+ *   status = 0 (reserved)
+ *   n      = number of elements the partial covers
+ *   acc    = the accumulator bits (integer value; fp32 +: float bits;
+ *            fp32 x / fp64 +: double bits; fp64 x: double-double hi, lo;
+ *            float min/max: order-preserving key and the max |x| bit pattern)
+ */
+typedef struct rd_record {
+  uint32_t tag;
+  uint32_t status;
+  uint64_t n;
+  uint64_t acc[2];
+} rd_record;
+
+/* ------------------------------------------------------------------ reduce
+ * reduce -- out[0] = x_0 (x) ... (x) x_{n-1} on one GPU.
+ *   x      device pointer to n contiguous elements of `dtype` (caller-owned,
+ *          read-only, any element-aligned offset).
+ *   n      element count, 0 <= n < 2^40.
+ *   out    device pointer to ONE element of `dtype` (caller-owned, written).
+ *   stream launch stream.
+ * One kernel launch (a single-pass persistent grid).
+ * Errors: INVALID_ARG (x NULL with n > 0, out NULL, bad enum), UNSUPPORTED,
+ * MISALIGNED (x or out), CUDA. */
+rd_status reduce(const void* x, size_t n, rd_dtype dtype, rd_op op, void* out, rd_stream_t stream);
+
+/* reduce_partial -- like reduce, but writes the un-narrowed partial of
+ * x[0..n) as one rd_record at device pointer `rec` (8-byte aligned).
+ * Used to split one logical reduction across shards, chunks or GPUs. */
+rd_status reduce_partial(const void* x, size_t n, rd_dtype dtype, rd_op op, rd_record* rec,
+                         rd_stream_t stream);
+
+/* rd_combine_records -- fold `count` device records in INDEX ORDER (rank or
+ * chunk order, so the result is deterministic) and write the narrowed value
+ * to device `out` (one element; may be NULL) and/or the folded record to
+ * device `rec_out` (may be NULL). If any record's tag differs from
+ * (dtype, op), *d_status (a device int, may be NULL) is set to
+ * RD_ERR_MISMATCH and `out` receives the empty result.
+ * The "second stage" of P:180 applied across blocks held by different
+ * owners. Errors: INVALID_ARG (recs NULL with count > 0, count < 0, both
+ * outputs NULL), UNSUPPORTED, CUDA. */
+rd_status rd_combine_records(const rd_record* recs, int count, rd_dtype dtype, rd_op op,
+                             void* out, rd_record* rec_out, int* d_status, rd_stream_t stream);
+
+/* reduce_host -- end-to-end reduction of a HOST array (pinned or pageable)
+ * on the current device: chunks are copied host->device on a copy stream,
+ * overlapped with reduce_partial on a compute stream (double-buffered), the
+ * chunk records are combined in chunk order, and the result is copied back
+ * to host `out_host` (one element). Synchronous: returns when *out_host is
+ * written. Device staging buffers are library-owned (freed by
+ * rd_release_workspaces). Errors: as reduce, plus CUDA. */
+rd_status reduce_host(const void* x_host, size_t n, rd_dtype dtype, rd_op op, void* out_host);
+
+/* ------------------------------------------------------------ multi-GPU
+ * One process per GPU. Rank r holds the r-th contiguous block of the
+ * logical array (rd_shard_range gives the canonical split). reduce_multi
+ * reduces the local block to a record, all-gathers the W records over NCCL
+ * (NVLink/NVSwitch), and folds them in RANK ORDER on every rank, so every
+ * rank gets the bitwise-identical result in its device `out`. n_local may
+ * differ across ranks and may be 0. Stream-ordered; a dtype/op disagreement
+ * between ranks is reported by the next rd_comm_check (all ranks see it). */
+typedef struct rd_comm* rd_comm_t;
+typedef struct { char internal[128]; } rd_unique_id;
+
+rd_status rd_get_unique_id(rd_unique_id* id);                  /* wraps ncclGetUniqueId */
+rd_status rd_comm_init(rd_comm_t* comm, int nranks, int rank, const rd_unique_id* id, int device);
+rd_status rd_comm_destroy(rd_comm_t comm);
+rd_status reduce_multi(const void* x_local, size_t n_local, rd_dtype dtype, rd_op op, void* out,
+                       rd_stream_t stream, rd_comm_t comm);
+/* Synchronises `stream`; returns RD_ERR_MISMATCH if any reduce_multi on this
+ * comm since the previous check saw records that disagree, and clears it. */
+rd_status rd_comm_check(rd_comm_t comm, rd_stream_t stream);
+/* Canonical contiguous split: rank r gets [begin, begin+count) with
+ * count = n/W + (r < n%W). Pure host function. */
+rd_status rd_shard_range(uint64_t n, int nranks, int rank, uint64_t* begin, uint64_t* count);
+
+/* ---------------------------------------------------------------- helpers */
+/* Host copy of the empty result (table above) into host_out (one element). */
+rd_status rd_identity(rd_dtype dtype, rd_op op, void* host_out);
+/* Frees the cached per-(device, stream) workspaces and reduce_host buffers.
+ * Must not race with in-flight calls. */
+rd_status rd_release_workspaces(void);
+const char* rd_status_string(rd_status s);
+/* Thread-local detail string for the last error on the calling thread. */
+const char* rd_last_error(void);
+
+/* ---------------------------------------------------- explicit launch control
+ * rd_reduce_ex -- reduce with an explicit kernel configuration, for the
+ * loads-in-flight ablation (the B200 form of PAPER.md Table 2)
+ * and for tests that force grid shapes. Any field 0 = the planner's choice.
+ *   variant   RD_VARIANT_AUTO, RD_VARIANT_VECTOR (grid-stride vector loads),
+ *             RD_VARIANT_PAPER (PAPER.md Listing "Unrolling the step 1",
+ *             F consecutive elements per work-item per iteration,
+ *             bounds handled by predication instead of the (i<len)*x mask)
+ *   vec_bytes 4, 8, 16 or 32 bytes per load (VECTOR variant)
+ *   unroll    loads in flight per thread per iteration (U; the paper's F)
+ *   grid      CTAs (clamped to [1, 4096])
+ * The chosen configuration is written to *info (may be NULL).
+ * Configurations without a compiled kernel return RD_ERR_UNSUPPORTED. */
+enum { RD_VARIANT_AUTO = 0, RD_VARIANT_VECTOR = 1, RD_VARIANT_PAPER = 2 };
+typedef struct { int32_t variant, vec_bytes, unroll, block, grid, reserved[3]; } rd_config;
+typedef struct {
+  int32_t variant, vec_bytes, unroll, block, grid, regs_per_thread, ctas_per_sm, reserved;
+  uint64_t head, nvec, tail;
+} rd_launch_info;
+rd_status rd_reduce_ex(const void* x, size_t n, rd_dtype dtype, rd_op op, void* out,
+                       rd_stream_t stream, const rd_config* cfg, rd_launch_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200REDUCE_H */

@@ -1,0 +1,218 @@
+"""paper_1710_07358_b200 -- B200-native (sm_100a) parallel reduction.
+
+Python binding of the C ABI in ``include/b200reduce.h`` (argument marshalling
+only; every step of the reduction runs in ``libb200reduce.so``). PyTorch is
+used for device memory, streams and process groups.
+
+    import torch, paper_1710_07358_b200 as rd
+    x = torch.rand(1 << 28, device="cuda")
+    s = rd.reduce(x, "sum")          # 0-d tensor on x.device
+
+The operation is x_0 (x) x_1 (x) ... (x) x_{n-1} for
+(x) in {sum, prod, min, max, and, or, xor} over int32/uint32/int64/float32/
+float64; semantics and tolerances are stated in include/b200reduce.h.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import ReduceError, check, lib
+
+__all__ = ["reduce", "reduce_partial", "combine_records", "reduce_host", "reduce_ex",
+           "reduce_multi", "Comm", "shard_range", "identity", "release_workspaces",
+           "ReduceError", "OPS", "RECORD_BYTES"]
+
+OPS = {"sum": _lib.RD_SUM, "prod": _lib.RD_PROD, "min": _lib.RD_MIN, "max": _lib.RD_MAX,
+       "and": _lib.RD_AND, "or": _lib.RD_OR, "xor": _lib.RD_XOR}
+DTYPE_NAMES = {"int32": _lib.RD_INT32, "uint32": _lib.RD_UINT32, "int64": _lib.RD_INT64,
+               "float32": _lib.RD_FLOAT32, "float64": _lib.RD_FLOAT64}
+RECORD_BYTES = 32
+VARIANTS = {"auto": _lib.RD_VARIANT_AUTO, "vector": _lib.RD_VARIANT_VECTOR, "paper": _lib.RD_VARIANT_PAPER}
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_name(dt) -> str:
+    s = str(dt)
+    return s.replace("torch.", "")
+
+
+def _dt(t) -> int:
+    name = _dtype_name(t.dtype)
+    if name not in DTYPE_NAMES:
+        raise TypeError(f"unsupported dtype {t.dtype}")
+    return DTYPE_NAMES[name]
+
+
+def _op(op: str) -> int:
+    if op not in OPS:
+        raise ValueError(f"unknown op {op!r}; expected one of {sorted(OPS)}")
+    return OPS[op]
+
+
+def _stream(t, stream):
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream(t.device).cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check_input(x):
+    if not x.is_cuda:
+        raise ValueError("x must be a CUDA tensor (use reduce_host for host arrays)")
+    if not x.is_contiguous():
+        raise ValueError("x must be contiguous")
+
+
+def reduce(x, op: str, out=None, stream=None):
+    """x_0 (x) ... (x) x_{n-1} over all elements of the contiguous CUDA tensor x."""
+    torch = _torch()
+    _check_input(x)
+    if out is None:
+        out = torch.empty((), dtype=x.dtype, device=x.device)
+    check(lib().reduce(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
+                       out.data_ptr(), _stream(x, stream)), "reduce")
+    return out
+
+
+def reduce_partial(x, op: str, rec=None, stream=None):
+    """Un-narrowed partial of x as one 32-byte rd_record (uint8 CUDA tensor)."""
+    torch = _torch()
+    _check_input(x)
+    if rec is None:
+        rec = torch.empty(RECORD_BYTES, dtype=torch.uint8, device=x.device)
+    check(lib().reduce_partial(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
+                               rec.data_ptr(), _stream(x, stream)), "reduce_partial")
+    return rec
+
+
+def combine_records(recs, dtype, op: str, out=None, rec_out=None, status=None, stream=None):
+    """Fold k records (a uint8 CUDA tensor of k*32 bytes) in index order."""
+    torch = _torch()
+    name = _dtype_name(dtype)
+    tdt = getattr(torch, name)
+    if recs.numel() % RECORD_BYTES:
+        raise ValueError("recs must hold whole 32-byte records")
+    if out is None and rec_out is None:
+        out = torch.empty((), dtype=tdt, device=recs.device)
+    check(lib().rd_combine_records(recs.data_ptr() if recs.numel() else None, recs.numel() // RECORD_BYTES,
+                                   DTYPE_NAMES[name], _op(op),
+                                   out.data_ptr() if out is not None else None,
+                                   rec_out.data_ptr() if rec_out is not None else None,
+                                   status.data_ptr() if status is not None else None,
+                                   _stream(recs, stream)), "rd_combine_records")
+    return out if out is not None else rec_out
+
+
+def reduce_host(x, op: str):
+    """End-to-end reduction of a host array (numpy array or CPU tensor; pinned
+    memory gives overlapped copies). Returns a numpy scalar."""
+    torch = _torch()
+    if isinstance(x, np.ndarray):
+        arr = np.ascontiguousarray(x)
+        name, ptr, n = arr.dtype.name, arr.ctypes.data, arr.size
+    else:
+        if x.is_cuda or not x.is_contiguous():
+            raise ValueError("reduce_host takes a contiguous host tensor")
+        name, ptr, n = _dtype_name(x.dtype), x.data_ptr(), x.numel()
+    if name not in DTYPE_NAMES:
+        raise TypeError(f"unsupported dtype {name}")
+    out = np.zeros(1, dtype=np.dtype(name))
+    check(lib().reduce_host(ptr if n else None, n, DTYPE_NAMES[name], _op(op), out.ctypes.data),
+          "reduce_host")
+    del torch
+    return out[0]
+
+
+def reduce_ex(x, op: str, variant: str = "auto", unroll: int = 0, vec_bytes: int = 0, grid: int = 0,
+              out=None, stream=None):
+    """reduce with an explicit kernel configuration; returns (out, info dict)."""
+    torch = _torch()
+    _check_input(x)
+    if out is None:
+        out = torch.empty((), dtype=x.dtype, device=x.device)
+    cfg = _lib.rd_config(VARIANTS[variant], vec_bytes, unroll, 0, grid)
+    info = _lib.rd_launch_info()
+    check(lib().rd_reduce_ex(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
+                             out.data_ptr(), _stream(x, stream), ctypes.byref(cfg), ctypes.byref(info)),
+          "rd_reduce_ex")
+    d = {k: getattr(info, k) for k, _ in _lib.rd_launch_info._fields_ if k != "reserved"}
+    d["variant"] = {v: k for k, v in VARIANTS.items()}[d["variant"]]
+    return out, d
+
+
+def shard_range(n: int, nranks: int, rank: int):
+    """Canonical contiguous split of n elements over nranks: (begin, count)."""
+    b, c = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib().rd_shard_range(n, nranks, rank, ctypes.byref(b), ctypes.byref(c)), "rd_shard_range")
+    return b.value, c.value
+
+
+def identity(dtype, op: str):
+    """The empty-input result (include/b200reduce.h table) as a numpy scalar."""
+    name = _dtype_name(dtype)
+    out = np.zeros(1, dtype=np.dtype(name))
+    check(lib().rd_identity(DTYPE_NAMES[name], _op(op), out.ctypes.data), "rd_identity")
+    return out[0]
+
+
+def release_workspaces():
+    check(lib().rd_release_workspaces(), "rd_release_workspaces")
+
+
+class Comm:
+    """One NCCL communicator per process/GPU for reduce_multi."""
+
+    def __init__(self, handle: int, nranks: int, rank: int, device: int):
+        self.handle, self.nranks, self.rank, self.device = handle, nranks, rank, device
+
+    @classmethod
+    def from_process_group(cls, group=None, device: int | None = None) -> "Comm":
+        """Create the communicator: rank 0 draws the NCCL unique id, which is
+        broadcast over the torch.distributed process group."""
+        torch = _torch()
+        import torch.distributed as dist
+        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        dev = torch.cuda.current_device() if device is None else device
+        uid = _lib.rd_unique_id()
+        if rank == 0:
+            check(lib().rd_get_unique_id(ctypes.byref(uid)), "rd_get_unique_id")
+        # the raw 128 bytes (uid.internal would stop at the first NUL)
+        obj = [ctypes.string_at(ctypes.addressof(uid), 128) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        ctypes.memmove(ctypes.addressof(uid), obj[0], 128)
+        h = ctypes.c_void_p()
+        check(lib().rd_comm_init(ctypes.byref(h), nranks, rank, ctypes.byref(uid), dev), "rd_comm_init")
+        return cls(h.value, nranks, rank, dev)
+
+    def reduce(self, x_local, op: str, out=None, stream=None):
+        return reduce_multi(x_local, op, self, out=out, stream=stream)
+
+    def check(self, stream=None):
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        check(lib().rd_comm_check(self.handle, st), "rd_comm_check")
+
+    def destroy(self):
+        if self.handle:
+            check(lib().rd_comm_destroy(self.handle), "rd_comm_destroy")
+            self.handle = None
+
+
+def reduce_multi(x_local, op: str, comm: Comm, out=None, stream=None):
+    """Sharded reduce: every rank passes its contiguous block (rank order);
+    every rank receives the bitwise-identical result."""
+    torch = _torch()
+    _check_input(x_local)
+    if out is None:
+        out = torch.empty((), dtype=x_local.dtype, device=x_local.device)
+    check(lib().reduce_multi(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
+                             _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
+                             comm.handle), "reduce_multi")
+    return out

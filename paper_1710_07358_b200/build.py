@@ -1,0 +1,87 @@
+"""Build the in-tree native libraries for sm_100a.
+
+    python -m paper_1710_07358_b200.build [--force]
+
+- paper_1710_07358_b200/libb200reduce.so   the product (C ABI: include/b200reduce.h)
+- inputs/libinputs_host.so, inputs/libinputs_device.so   seeded generators
+- oracle/liboracle.so                       the CPU checker (test infrastructure;
+                                            building it is not using it)
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import glob
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+OBJ = os.path.join(ROOT, "build", "obj")
+LIB = os.path.join(PKG, "libb200reduce.so")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dir() -> str:
+    import nvidia.nccl
+    return list(nvidia.nccl.__path__)[0]
+
+
+def _deps():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) +
+                  [os.path.join(INCLUDE, "b200reduce.h")])
+
+
+def _stale(out, srcs):
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(s) > t for s in srcs)
+
+
+def _compile(src: str, force: bool) -> str:
+    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    if force or _stale(obj, [src] + _deps()):
+        cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+               "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(nccl_dir(), "include"),
+               "-c", src, "-o", obj + ".tmp"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        with open(obj + ".ptxas.log", "w") as f:
+            f.write(r.stdout + r.stderr)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-6000:]}")
+        os.replace(obj + ".tmp", obj)
+    return obj
+
+
+def build_library(force: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    with cf.ThreadPoolExecutor(max_workers=max(2, os.cpu_count() or 2)) as ex:
+        objs = list(ex.map(lambda s: _compile(s, force), srcs))
+    if force or _stale(LIB, objs):
+        nd = nccl_dir()
+        cmd = ["nvcc", *ARCH, "-shared", "-o", LIB + ".tmp", *objs,
+               "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+               "-Xlinker", f"-rpath={os.path.join(nd, 'lib')}"]
+        subprocess.check_call(cmd)
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+def build_all(force: bool = False) -> None:
+    sys.path.insert(0, ROOT)
+    import inputs
+    import oracle
+    with cf.ThreadPoolExecutor(max_workers=3) as ex:
+        futs = [ex.submit(build_library, force), ex.submit(inputs.build_device, force),
+                ex.submit(inputs.build_host, force), ex.submit(oracle.build, force)]
+        for f in futs:
+            f.result()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)
+    print(LIB)

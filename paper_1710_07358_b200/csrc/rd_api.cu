@@ -1,0 +1,334 @@
+// rd_api.cu -- the C ABI (include/b200reduce.h): validation, the launch
+// planner and the per-(device, stream) workspace.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+
+#include "b200reduce.h"
+#include "rd_internal.h"
+#include "rd_registry.h"
+
+namespace rd {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+rd_status cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+  return RD_ERR_CUDA;
+}
+
+int dtype_size(int dtype) {
+  return (dtype == RD_INT64 || dtype == RD_FLOAT64) ? 8 : 4;
+}
+
+rd_status check_dtype_op(int dtype, int op) {
+  if (dtype < RD_INT32 || dtype > RD_FLOAT64) { set_error("unknown dtype"); return RD_ERR_INVALID_ARG; }
+  if (op < RD_SUM || op > RD_XOR) { set_error("unknown op"); return RD_ERR_INVALID_ARG; }
+  if ((dtype == RD_FLOAT32 || dtype == RD_FLOAT64) && op >= RD_AND) {
+    set_error("bitwise op on a float dtype");
+    return RD_ERR_UNSUPPORTED;
+  }
+  return RD_OK;
+}
+
+// ------------------------------------------------------------------ workspace
+namespace {
+
+struct Workspace {
+  Slot* partials = nullptr;   // kMaxGrid slots
+  unsigned* ticket = nullptr; // one counter, zero between launches
+};
+
+struct DeviceInfo {
+  int sms = 0;
+};
+
+std::mutex g_mu;
+std::map<std::pair<int, uintptr_t>, Workspace> g_ws;
+std::map<int, DeviceInfo> g_dev;
+std::map<std::pair<int, const void*>, int> g_occ;   // (device, kernel) -> CTAs/SM
+std::map<std::pair<int, const void*>, int> g_regs;  // (device, kernel) -> regs/thread
+
+rd_status get_workspace(int dev, cudaStream_t stream, Workspace* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, (uintptr_t)stream);
+  auto it = g_ws.find(key);
+  if (it != g_ws.end()) { *out = it->second; return RD_OK; }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+    set_error("first call on a stream must happen outside CUDA graph capture (workspace allocation)");
+    return RD_ERR_CUDA;
+  }
+  Workspace w;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, sizeof(Slot) * kMaxGrid + 256);
+  if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
+  e = cudaMemset(p, 0, sizeof(Slot) * kMaxGrid + 256);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "workspace init"); }
+  w.partials = (Slot*)p;
+  w.ticket = (unsigned*)((char*)p + sizeof(Slot) * kMaxGrid);
+  g_ws[key] = w;
+  *out = w;
+  return RD_OK;
+}
+
+rd_status device_info(int dev, DeviceInfo* out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_dev.find(dev);
+  if (it != g_dev.end()) { *out = it->second; return RD_OK; }
+  DeviceInfo d;
+  cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  g_dev[dev] = d;
+  *out = d;
+  return RD_OK;
+}
+
+rd_status occupancy(int dev, const KernelRef& k, int* ctas, int* regs) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, (const void*)k.fn);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) { *ctas = it->second; *regs = g_regs[key]; return RD_OK; }
+  int c = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k.fn, k.block, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, k.fn);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes");
+  if (c < 1) c = 1;
+  g_occ[key] = c;
+  g_regs[key] = fa.numRegs;
+  *ctas = c;
+  *regs = fa.numRegs;
+  return RD_OK;
+}
+
+bool lookup(int dtype, int op, int variant, int unroll, int vec_bytes, KernelRef* r) {
+  if (lookup_ablation(dtype, op, variant, unroll, vec_bytes, r)) return true;
+  if (dtype == RD_FLOAT32 || dtype == RD_FLOAT64) return lookup_float(dtype, op, variant, unroll, vec_bytes, r);
+  return lookup_int(dtype, op, variant, unroll, vec_bytes, r);
+}
+
+}  // namespace
+
+// a0: validate, plan, launch.
+rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, void* out,
+                        rd_record* rec, cudaStream_t stream, const rd_config* cfg,
+                        rd_launch_info* info) {
+  rd_status st = check_dtype_op(dtype, op);
+  if (st != RD_OK) return st;
+  const int s = dtype_size(dtype);
+  if (x == nullptr && n > 0) { set_error("x is NULL"); return RD_ERR_INVALID_ARG; }
+  if (mode == 0 && out == nullptr) { set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
+  if (mode == 1 && rec == nullptr) { set_error("rec is NULL"); return RD_ERR_INVALID_ARG; }
+  if ((uintptr_t)x % s != 0) { set_error("x is not aligned to sizeof(dtype)"); return RD_ERR_MISALIGNED; }
+  if (mode == 0 && (uintptr_t)out % s != 0) { set_error("out is not aligned to sizeof(dtype)"); return RD_ERR_MISALIGNED; }
+  if (mode == 1 && (uintptr_t)rec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
+  if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
+
+  const int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
+  const int unroll = cfg ? cfg->unroll : 0;
+  const int vec_bytes = cfg ? cfg->vec_bytes : 0;
+  if (cfg && (cfg->block != 0 && cfg->block != kBlock)) {
+    set_error("only block = 256 is compiled");
+    return RD_ERR_UNSUPPORTED;
+  }
+  if (variant < RD_VARIANT_AUTO || variant > RD_VARIANT_PAPER || unroll < 0 || vec_bytes < 0 ||
+      (cfg && cfg->grid < 0)) {
+    set_error("bad rd_config");
+    return RD_ERR_INVALID_ARG;
+  }
+  if (vec_bytes && vec_bytes < s) { set_error("vec_bytes < sizeof(dtype)"); return RD_ERR_INVALID_ARG; }
+  KernelRef k;
+  if (!lookup(dtype, op, variant, unroll, vec_bytes, &k)) {
+    set_error("no compiled kernel for this (dtype, op, variant, unroll, vec_bytes)");
+    return RD_ERR_UNSUPPORTED;
+  }
+
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  DeviceInfo di;
+  if ((st = device_info(dev, &di)) != RD_OK) return st;
+  int occ = 1, regs = 0;
+  if ((st = occupancy(dev, k, &occ, &regs)) != RD_OK) return st;
+  Workspace ws;
+  if ((st = get_workspace(dev, stream, &ws)) != RD_OK) return st;
+
+  KArgs a;
+  a.x = (const unsigned char*)x;
+  a.n = n;
+  uint64_t units;  // work units handed out by the grid-stride loop
+  if (k.variant == RD_VARIANT_VECTOR) {
+    const uint64_t L = (uint64_t)(k.vec_bytes / s);
+    const uint64_t mis = (uint64_t)((uintptr_t)x % (uintptr_t)k.vec_bytes);
+    uint64_t head = ((k.vec_bytes - mis) % k.vec_bytes) / s;
+    if (head > n) head = n;
+    a.head = head;
+    a.nvec = (n - head) / L;
+    a.tail_start = head + a.nvec * L;
+    a.tail = n - a.tail_start;
+    units = a.nvec;
+  } else {  // PAPER: F consecutive elements per work-item
+    a.head = 0;
+    a.nvec = 0;
+    a.tail_start = n;
+    a.tail = 0;
+    units = (n + k.unroll - 1) / k.unroll;
+    k.unroll = k.unroll;
+  }
+  // Persistent grid: at most the CTAs that are resident
+  // at once, fewer when there is less work than one unrolled pass.
+  const uint64_t per_cta = (uint64_t)k.block * (k.variant == RD_VARIANT_VECTOR ? k.unroll : 1);
+  uint64_t g = (uint64_t)di.sms * occ;
+  uint64_t need = (units + per_cta - 1) / per_cta;
+  if (need < 1) need = 1;
+  if (g > need) g = need;
+  if (cfg && cfg->grid > 0) g = (uint64_t)cfg->grid;
+  if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
+  if (g < 1) g = 1;
+
+  a.out = out;
+  a.rec = rec;
+  a.partials = ws.partials;
+  a.ticket = ws.ticket;
+  a.tag = record_tag(dtype, op);
+  a.mode = mode;
+
+  k.fn<<<(unsigned)g, k.block, 0, stream>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->variant = k.variant;
+    info->vec_bytes = k.vec_bytes;
+    info->unroll = k.unroll;
+    info->block = k.block;
+    info->grid = (int32_t)g;
+    info->regs_per_thread = regs;
+    info->ctas_per_sm = occ;
+    info->head = a.head;
+    info->nvec = a.nvec;
+    info->tail = a.tail;
+  }
+  return RD_OK;
+}
+
+rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, void* out,
+                         rd_record* rec_out, int* d_status, cudaStream_t stream) {
+  rd_status st = check_dtype_op(dtype, op);
+  if (st != RD_OK) return st;
+  if (count < 0 || (count > 0 && recs == nullptr)) { set_error("bad recs/count"); return RD_ERR_INVALID_ARG; }
+  if (out == nullptr && rec_out == nullptr) { set_error("no output"); return RD_ERR_INVALID_ARG; }
+  if (out && (uintptr_t)out % dtype_size(dtype)) { set_error("out misaligned"); return RD_ERR_MISALIGNED; }
+  CombineFn fn = lookup_combine(dtype, op);
+  if (!fn) { set_error("no combine kernel"); return RD_ERR_UNSUPPORTED; }
+  fn<<<1, 32, 0, stream>>>(recs, count, record_tag(dtype, op), out, rec_out, d_status);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "combine kernel launch");
+  return RD_OK;
+}
+
+static void release_all_workspaces() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto& kv : g_ws) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(kv.first.first);
+    cudaFree(kv.second.partials);
+    cudaSetDevice(cur);
+  }
+  g_ws.clear();
+}
+
+}  // namespace rd
+
+// ====================================================================== C ABI
+extern "C" {
+
+rd_status reduce(const void* x, size_t n, rd_dtype dtype, rd_op op, void* out, rd_stream_t stream) {
+  return rd::launch_reduce(x, n, dtype, op, 0, out, nullptr, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+rd_status reduce_partial(const void* x, size_t n, rd_dtype dtype, rd_op op, rd_record* rec,
+                         rd_stream_t stream) {
+  return rd::launch_reduce(x, n, dtype, op, 1, nullptr, rec, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+rd_status rd_reduce_ex(const void* x, size_t n, rd_dtype dtype, rd_op op, void* out,
+                       rd_stream_t stream, const rd_config* cfg, rd_launch_info* info) {
+  return rd::launch_reduce(x, n, dtype, op, 0, out, nullptr, (cudaStream_t)stream, cfg, info);
+}
+
+rd_status rd_combine_records(const rd_record* recs, int count, rd_dtype dtype, rd_op op, void* out,
+                             rd_record* rec_out, int* d_status, rd_stream_t stream) {
+  return rd::launch_combine(recs, count, dtype, op, out, rec_out, d_status, (cudaStream_t)stream);
+}
+
+rd_status rd_identity(rd_dtype dtype, rd_op op, void* host_out) {
+  rd_status st = rd::check_dtype_op(dtype, op);
+  if (st != RD_OK) return st;
+  if (!host_out) { rd::set_error("host_out is NULL"); return RD_ERR_INVALID_ARG; }
+  if (dtype == RD_FLOAT32 || dtype == RD_FLOAT64) {
+    const double inf = __builtin_huge_val();
+    double v = op == RD_SUM ? 0.0 : op == RD_PROD ? 1.0 : op == RD_MIN ? inf : -inf;
+    if (dtype == RD_FLOAT32) { float f = (float)v; std::memcpy(host_out, &f, 4); }
+    else std::memcpy(host_out, &v, 8);
+    return RD_OK;
+  }
+  const bool w64 = dtype == RD_INT64;
+  uint64_t v = 0;
+  switch (op) {
+    case RD_PROD: v = 1; break;
+    case RD_AND: v = ~0ull; break;
+    case RD_MIN: v = dtype == RD_UINT32 ? 0xFFFFFFFFull : (w64 ? 0x7FFFFFFFFFFFFFFFull : 0x7FFFFFFFull); break;
+    case RD_MAX: v = dtype == RD_UINT32 ? 0ull : (w64 ? 0x8000000000000000ull : 0x80000000ull); break;
+    default: v = 0; break;
+  }
+  if (w64) std::memcpy(host_out, &v, 8);
+  else { uint32_t u = (uint32_t)v; std::memcpy(host_out, &u, 4); }
+  return RD_OK;
+}
+
+rd_status rd_shard_range(uint64_t n, int nranks, int rank, uint64_t* begin, uint64_t* count) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !begin || !count) {
+    rd::set_error("bad shard arguments");
+    return RD_ERR_INVALID_ARG;
+  }
+  const uint64_t W = (uint64_t)nranks, r = (uint64_t)rank;
+  const uint64_t q = n / W, rem = n % W;
+  *begin = r * q + (r < rem ? r : rem);
+  *count = q + (r < rem ? 1 : 0);
+  return RD_OK;
+}
+
+rd_status rd_release_workspaces(void) {
+  rd::release_all_workspaces();
+  rd::release_host_pipelines();
+  return RD_OK;
+}
+
+const char* rd_status_string(rd_status s) {
+  switch (s) {
+    case RD_OK: return "RD_OK";
+    case RD_ERR_INVALID_ARG: return "RD_ERR_INVALID_ARG";
+    case RD_ERR_UNSUPPORTED: return "RD_ERR_UNSUPPORTED";
+    case RD_ERR_MISALIGNED: return "RD_ERR_MISALIGNED";
+    case RD_ERR_CUDA: return "RD_ERR_CUDA";
+    case RD_ERR_NCCL: return "RD_ERR_NCCL";
+    case RD_ERR_MISMATCH: return "RD_ERR_MISMATCH";
+    default: return "RD_ERR_UNKNOWN";
+  }
+}
+
+const char* rd_last_error(void) { return rd::g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,33 @@
+// rd_internal.h -- host-side pieces shared by the library's translation units
+// (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "b200reduce.h"
+
+namespace rd {
+
+// thread-local detail for rd_last_error()
+void set_error(const std::string& msg);
+rd_status cuda_fail(cudaError_t e, const char* what);
+
+// argument checks shared by every entry point (synchronous, enqueue nothing)
+rd_status check_dtype_op(int dtype, int op);
+int dtype_size(int dtype);
+
+// Plan + launch one reduction of x[0..n) (a0-a7). mode 0 writes one element
+// to `out`, mode 1 writes one rd_record to `rec`.
+rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, void* out,
+                        rd_record* rec, cudaStream_t stream, const rd_config* cfg,
+                        rd_launch_info* info);
+
+// Launch the record-combine kernel (N4).
+rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, void* out,
+                         rd_record* rec_out, int* d_status, cudaStream_t stream);
+
+// per-(device) cleanup hooks of the other translation units
+void release_host_pipelines();
+
+}  // namespace rd

@@ -1,0 +1,264 @@
+// rd_kernels.cuh -- the sm_100a reduction kernels.
+//
+// rd_vector_kernel: single-pass persistent reduction.
+//   a1  Step 1 of the two-stage reduction (Listing 1 ln042-045,
+//       and the paper's unrolled Step 1): each thread walks the
+//       32-byte-aligned body grid-stride ("skipping GS positions at every
+//       step"), issuing U independent 256-bit non-allocating loads
+//       (LDG.E.ENL2.256) before folding them into L = VB/sizeof(T) independent
+//       accumulators -- the paper's unrolling factor F realised as loads in
+//       flight rather than as scalar index arithmetic.
+//   a2  head/tail (< VB/sizeof(T) elements each) by predicated scalar loads:
+//       never out of bounds (the listing's (i<len)*x read is not reproduced).
+//   a3  in-thread fold of the L lane accumulators.
+//   a4  warp combine: redux.sync or a shfl_xor butterfly.
+//   a5  block combine ("Step 3"): warp leaders -> smem[warp],
+//       ONE __syncthreads, warp 0 folds (the barrier-free tree of P:317-326 is
+//       a cross-warp race on sm_100 and is not reproduced).
+//   a6  grid combine (replaces the second launch): CTA b stores its
+//       partial, fences, takes an atomic ticket; the CTA that draws the last
+//       ticket folds partials[0..G) in index order and resets the ticket.
+//   a7  narrow Acc -> T once and store (or emit an rd_record).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "rd_ops.cuh"
+
+namespace rd {
+
+struct KArgs {
+  const unsigned char* x;   // element 0
+  uint64_t n;               // elements
+  uint64_t head;            // elements before the VB-aligned body
+  uint64_t nvec;            // VB-byte vectors in the body
+  uint64_t tail_start;      // first element after the body
+  uint64_t tail;            // elements after the body
+  void* out;                // mode 0: one element of T
+  rd_record* rec;           // mode 1: one record
+  Slot* partials;           // gridDim.x slots (workspace)
+  unsigned* ticket;         // zero between launches (workspace)
+  uint32_t tag;             // record tag
+  int mode;                 // 0 = value, 1 = record
+};
+
+// ---------------------------------------------------------------- loads
+template <int VB> struct Vec { uint32_t w[VB / 4]; };
+
+// Streaming, read-only, no L1 allocation; L2 fetches a 256-byte sector group.
+template <int VB>
+__device__ __forceinline__ Vec<VB> ldg_stream(const unsigned char* p) {
+  Vec<VB> v;
+  if constexpr (VB == 32) {
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]),
+          "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]), "=r"(v.w[7])
+        : "l"(p));
+  } else if constexpr (VB == 16) {
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+        : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3])
+        : "l"(p));
+  } else if constexpr (VB == 8) {
+    asm("ld.global.nc.L1::no_allocate.L2::256B.v2.u32 {%0,%1}, [%2];"
+        : "=r"(v.w[0]), "=r"(v.w[1])
+        : "l"(p));
+  } else {
+    static_assert(VB == 4, "VB");
+    asm("ld.global.nc.L1::no_allocate.L2::256B.u32 %0, [%1];" : "=r"(v.w[0]) : "l"(p));
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T ldg_scalar(const unsigned char* p) {
+  return __ldg(reinterpret_cast<const T*>(p));
+}
+
+template <typename T, int VB>
+__device__ __forceinline__ T lane(const Vec<VB>& v, int l) {
+  if constexpr (sizeof(T) == 4) {
+    uint32_t u = v.w[l];
+    T t;
+    memcpy(&t, &u, 4);
+    return t;
+  } else {
+    uint64_t u = ((uint64_t)v.w[2 * l + 1] << 32) | v.w[2 * l];
+    T t;
+    memcpy(&t, &u, 8);
+    return t;
+  }
+}
+
+// ---------------------------------------------------------- block combine
+template <class OpT, int B>
+__device__ __forceinline__ typename OpT::Acc block_reduce(typename OpT::Acc a, typename OpT::Acc* smem) {
+  static_assert(B % 32 == 0 && B <= 1024, "B");
+  a = OpT::warp_reduce(a);
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if constexpr (B > 32) {
+    if (ln == 0) smem[warp] = a;
+    __syncthreads();
+    if (warp == 0) {
+      a = (ln < B / 32) ? smem[ln] : OpT::identity();
+      a = OpT::warp_reduce(a);
+    }
+  }
+  return a;  // valid in thread 0
+}
+
+template <class OpT>
+__device__ __forceinline__ void finish(const typename OpT::Acc& a, const KArgs& args) {
+  if (args.mode == 0) {
+    if (args.n == 0) OpT::store_empty(args.out);
+    else OpT::store(a, args.out);
+  } else {
+    Slot s = OpT::pack(a);
+    args.rec->tag = args.tag;
+    args.rec->status = 0;
+    args.rec->n = args.n;
+    args.rec->acc[0] = s.a;
+    args.rec->acc[1] = s.b;
+  }
+}
+
+// a6: one partial per CTA, the last CTA to arrive folds them in index order.
+template <class OpT, int B>
+__device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& args,
+                                             typename OpT::Acc* smem) {
+  using Acc = typename OpT::Acc;
+  if (gridDim.x == 1) {
+    if (threadIdx.x == 0) finish<OpT>(a, args);
+    return;
+  }
+  __shared__ unsigned s_last;
+  if (threadIdx.x == 0) {
+    Slot s = OpT::pack(a);
+    __stcg(reinterpret_cast<ulonglong2*>(args.partials + blockIdx.x), make_ulonglong2(s.a, s.b));
+    __threadfence();                                   // release the partial
+    unsigned t = atomicAdd(args.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();                                     // acquire the other partials
+  Acc b = OpT::identity();
+  for (unsigned j = threadIdx.x; j < gridDim.x; j += B) {
+    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(args.partials + j));
+    b = OpT::combine(b, OpT::unpack(Slot{v.x, v.y}));
+  }
+  b = block_reduce<OpT, B>(b, smem);
+  if (threadIdx.x == 0) {
+    finish<OpT>(b, args);
+    *args.ticket = 0u;                                 // reusable by the next launch
+  }
+}
+
+// ---------------------------------------------------------------- a1-a7
+template <class OpT, int B, int U, int VB>
+__global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
+  using T = typename OpT::T;
+  using Acc = typename OpT::Acc;
+  constexpr int L = VB / (int)sizeof(T);
+  static_assert(L >= 1, "vector narrower than the element");
+  __shared__ Acc smem[32];
+
+  Acc acc[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) acc[l] = OpT::identity();
+
+  const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * B;
+  const unsigned char* body = args.x + args.head * sizeof(T);
+  const uint64_t nvec = args.nvec;
+  uint64_t i = tid;
+  if constexpr (U > 1) {
+    for (; i + (uint64_t)(U - 1) * stride < nvec; i += (uint64_t)U * stride) {
+      Vec<VB> v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, VB>(v[u], l));
+    }
+  }
+  for (; i < nvec; i += stride) {
+    Vec<VB> v = ldg_stream<VB>(body + i * VB);
+#pragma unroll
+    for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, VB>(v, l));
+  }
+  // a2: head and tail stragglers
+  if (tid < args.head) acc[0] = OpT::fold(acc[0], ldg_scalar<T>(args.x + tid * sizeof(T)));
+  if (tid < args.tail) acc[L - 1] = OpT::fold(acc[L - 1], ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T)));
+  // a3
+  Acc a = acc[0];
+#pragma unroll
+  for (int l = 1; l < L; ++l) a = OpT::combine(a, acc[l]);
+  // a4, a5
+  a = block_reduce<OpT, B>(a, smem);
+  __syncthreads();  // smem is reused by the grid combine
+  // a6, a7
+  grid_combine<OpT, B>(a, args, smem);
+}
+
+// PAPER.md Listing "Unrolling the step 1", transcribed: work-item
+// g reads the F CONSECUTIVE elements iPos..iPos+F-1, iPos = g*F + k*GS*F.
+// The listing's algebraic mask (i<len)*x is replaced by predication
+// with the op's identity (the mask reads out of bounds and is not an identity
+// for x/min/max or for inf/NaN). Used for the F-sweep ablation.
+template <class OpT, int B, int F>
+__global__ void __launch_bounds__(B) rd_paper_kernel(const KArgs args) {
+  using T = typename OpT::T;
+  using Acc = typename OpT::Acc;
+  __shared__ Acc smem[32];
+  Acc acc = OpT::identity();
+  const uint64_t gid = (uint64_t)blockIdx.x * B + threadIdx.x;
+  const uint64_t gs = (uint64_t)gridDim.x * B;
+  const T* x = reinterpret_cast<const T*>(args.x);
+  const uint64_t n = args.n;
+  for (uint64_t pos = gid * F; pos < n; pos += gs * F) {
+    T v[F];
+#pragma unroll
+    for (int k = 0; k < F; ++k) v[k] = (pos + k < n) ? __ldg(x + pos + k) : T{};
+#pragma unroll
+    for (int k = 0; k < F; ++k)
+      if (pos + k < n) acc = OpT::fold(acc, v[k]);
+  }
+  acc = block_reduce<OpT, B>(acc, smem);
+  __syncthreads();
+  grid_combine<OpT, B>(acc, args, smem);
+}
+
+// ------------------------------------------------------ record combine (N4)
+// Folds records in index order with one thread (count is the number of ranks
+// or chunks: small); checks every tag.
+template <class OpT>
+__global__ void rd_combine_kernel(const rd_record* recs, int count, uint32_t tag, void* out,
+                                  rd_record* rec_out, int* d_status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  using Acc = typename OpT::Acc;
+  Acc a = OpT::identity();
+  uint64_t n = 0;
+  bool bad = false;
+  for (int r = 0; r < count; ++r) {
+    const rd_record rc = recs[r];
+    if (rc.tag != tag) { bad = true; continue; }
+    n += rc.n;
+    a = OpT::combine(a, OpT::unpack(Slot{rc.acc[0], rc.acc[1]}));
+  }
+  if (bad && d_status) *d_status = (int)RD_ERR_MISMATCH;
+  if (out) {
+    if (n == 0 || bad) OpT::store_empty(out);
+    else OpT::store(a, out);
+  }
+  if (rec_out) {
+    Slot s = OpT::pack(a);
+    rec_out->tag = tag;
+    rec_out->status = bad ? (uint32_t)RD_ERR_MISMATCH : 0u;
+    rec_out->n = n;
+    rec_out->acc[0] = s.a;
+    rec_out->acc[1] = s.b;
+  }
+}
+
+}  // namespace rd

@@ -1,0 +1,277 @@
+// rd_ops.cuh -- the combiner (x) of PAPER.md P:23 for every (dtype, op) pair,
+// as device-side traits used by every kernel of the library.
+//
+// Each trait defines
+//   T         storage type of one element (raw bit pattern for integers)
+//   Acc       accumulator type (wider for fp32 x and fp64 x; see b200reduce.h)
+//   identity  the padding element: combine(identity, a) == a for every a
+//             (Algorithm 1's initial accumulator; -0.0 for float +,
+//             because +0.0 is not an identity for -0.0)
+//   fold      acc (x) x_i for one element (the body of Algorithm 1's loop)
+//   combine   acc (x) acc
+//   warp_reduce  butterfly over the 32 lanes (Luitjens' SHFL tree),
+//             or redux.sync for 32-bit integer add/min/max/and/or/xor
+//   store     narrow to T with one rounding and write one element
+//   store_empty  the empty-input result (b200reduce.h table)
+//   pack/unpack  16-byte slot for partials and rd_record.acc
+#pragma once
+#include <cstdint>
+#include <type_traits>
+#include <cuda_runtime.h>
+
+#include "b200reduce.h"
+
+namespace rd {
+
+struct Slot { uint64_t a, b; };
+
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  uint32_t lo = (uint32_t)v, hi = (uint32_t)(v >> 32);
+  lo = __shfl_xor_sync(0xffffffffu, lo, m);
+  hi = __shfl_xor_sync(0xffffffffu, hi, m);
+  return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ double shfl_xor_f64(double v, int m) {
+  return __longlong_as_double((long long)shfl_xor_u64((uint64_t)__double_as_longlong(v), m));
+}
+
+// ------------------------------------------------------------------ integers
+template <typename U, rd_op OP, bool SIGNED>
+struct IntOp {
+  using T = U;
+  using Acc = U;
+  static constexpr bool kFloat = false;
+  using S = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
+
+  __device__ __forceinline__ static Acc identity() {
+    if (OP == RD_SUM || OP == RD_OR || OP == RD_XOR) return (U)0;
+    if (OP == RD_PROD) return (U)1;
+    if (OP == RD_AND) return (U)~(U)0;
+    constexpr U smax = (U)(~(U)0) >> 1;         // 0x7fff..
+    if (OP == RD_MIN) return SIGNED ? smax : (U)~(U)0;
+    /* RD_MAX */ return SIGNED ? (U)(smax + (U)1) : (U)0;
+  }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) {
+    if (OP == RD_SUM) return a + b;                       // wraps mod 2^w
+    if (OP == RD_PROD) return a * b;                      // wraps mod 2^w
+    if (OP == RD_AND) return a & b;
+    if (OP == RD_OR) return a | b;
+    if (OP == RD_XOR) return a ^ b;
+    if (OP == RD_MIN) {
+      if (SIGNED) return ((S)a < (S)b) ? a : b;
+      return a < b ? a : b;
+    }
+    if (SIGNED) return ((S)a > (S)b) ? a : b;
+    return a > b ? a : b;
+  }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) { return combine(a, x); }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+    if constexpr (sizeof(U) == 4 && OP != RD_PROD) {
+      // redux.sync (sm_80+): one instruction for the whole warp
+      if (OP == RD_SUM) return __reduce_add_sync(0xffffffffu, (unsigned)a);
+      if (OP == RD_AND) return __reduce_and_sync(0xffffffffu, (unsigned)a);
+      if (OP == RD_OR) return __reduce_or_sync(0xffffffffu, (unsigned)a);
+      if (OP == RD_XOR) return __reduce_xor_sync(0xffffffffu, (unsigned)a);
+      if (OP == RD_MIN)
+        return SIGNED ? (U)__reduce_min_sync(0xffffffffu, (int)a) : (U)__reduce_min_sync(0xffffffffu, (unsigned)a);
+      return SIGNED ? (U)__reduce_max_sync(0xffffffffu, (int)a) : (U)__reduce_max_sync(0xffffffffu, (unsigned)a);
+    } else {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        U o = (sizeof(U) == 4) ? (U)__shfl_xor_sync(0xffffffffu, (uint32_t)a, m) : (U)shfl_xor_u64((uint64_t)a, m);
+        a = combine(a, o);
+      }
+      return a;
+    }
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) { *(T*)out = a; }
+  __device__ __forceinline__ static void store_empty(void* out) { *(T*)out = identity(); }
+  __device__ __forceinline__ static Slot pack(Acc a) { return Slot{(uint64_t)a, 0}; }
+  __device__ __forceinline__ static Acc unpack(Slot s) { return (Acc)s.a; }
+};
+
+// ------------------------------------------------------------ float32 / float64 +
+template <typename F>
+struct FloatSum {
+  using T = F;
+  using Acc = F;
+  static constexpr bool kFloat = true;
+  __device__ __forceinline__ static Acc identity() { return (F)(-0.0); }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) { return a + b; }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) { return a + x; }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      if constexpr (sizeof(F) == 4) a = a + __shfl_xor_sync(0xffffffffu, a, m);
+      else a = a + shfl_xor_f64(a, m);
+    }
+    return a;
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) { *(T*)out = a; }
+  __device__ __forceinline__ static void store_empty(void* out) { *(T*)out = (F)0.0; }
+  __device__ __forceinline__ static Slot pack(Acc a) {
+    if constexpr (sizeof(F) == 4) return Slot{(uint64_t)__float_as_uint(a), 0};
+    else return Slot{(uint64_t)__double_as_longlong(a), 0};
+  }
+  __device__ __forceinline__ static Acc unpack(Slot s) {
+    if constexpr (sizeof(F) == 4) return __uint_as_float((uint32_t)s.a);
+    else return __longlong_as_double((long long)s.a);
+  }
+};
+
+// ------------------------------------------------- float32 x (fp64 accumulator)
+struct Float32Prod {
+  using T = float;
+  using Acc = double;
+  static constexpr bool kFloat = true;
+  __device__ __forceinline__ static Acc identity() { return 1.0; }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) { return __dmul_rn(a, b); }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) { return __dmul_rn(a, (double)x); }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) a = __dmul_rn(a, shfl_xor_f64(a, m));
+    return a;
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) { *(float*)out = __double2float_rn(a); }
+  __device__ __forceinline__ static void store_empty(void* out) { *(float*)out = 1.0f; }
+  __device__ __forceinline__ static Slot pack(Acc a) { return Slot{(uint64_t)__double_as_longlong(a), 0}; }
+  __device__ __forceinline__ static Acc unpack(Slot s) { return __longlong_as_double((long long)s.a); }
+};
+
+// ---------------------------------------- float64 x (double-double accumulator)
+struct DD { double hi, lo; };
+
+struct Float64Prod {
+  using T = double;
+  using Acc = DD;
+  static constexpr bool kFloat = true;
+  __device__ __forceinline__ static Acc identity() { return DD{1.0, 0.0}; }
+  // renormalise p + e (|e| <= ulp(p)/2-ish): Fast2Sum; keep plain p for
+  // zero / inf / NaN products where the error term is meaningless.
+  __device__ __forceinline__ static Acc renorm(double p, double e) {
+    double s = __dadd_rn(p, e);
+    double l = __dsub_rn(e, __dsub_rn(s, p));
+    bool ok = (p != 0.0) && (fabs(p) < __longlong_as_double(0x7ff0000000000000LL));
+    return ok ? DD{s, l} : DD{p, 0.0};
+  }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) {
+    double p = __dmul_rn(a.hi, x);
+    double e = __fma_rn(a.hi, x, -p);       // exact error of a.hi * x (TwoProduct)
+    e = __fma_rn(a.lo, x, e);
+    return renorm(p, e);
+  }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) {
+    double p = __dmul_rn(a.hi, b.hi);
+    double e = __fma_rn(a.hi, b.hi, -p);
+    e = __fma_rn(a.hi, b.lo, e);
+    e = __fma_rn(a.lo, b.hi, e);
+    return renorm(p, e);
+  }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      DD o{shfl_xor_f64(a.hi, m), shfl_xor_f64(a.lo, m)};
+      a = combine(a, o);
+    }
+    return a;
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) { *(double*)out = a.hi; }
+  __device__ __forceinline__ static void store_empty(void* out) { *(double*)out = 1.0; }
+  __device__ __forceinline__ static Slot pack(Acc a) {
+    return Slot{(uint64_t)__double_as_longlong(a.hi), (uint64_t)__double_as_longlong(a.lo)};
+  }
+  __device__ __forceinline__ static Acc unpack(Slot s) {
+    return DD{__longlong_as_double((long long)s.a), __longlong_as_double((long long)s.b)};
+  }
+};
+
+// ------------------------------------------------------------- float min / max
+// IEEE 754-2019 minimum/maximum, bit-exact and order-independent:
+//   key(x)  = the float's bits with the magnitude bits flipped when negative,
+//             compared as a signed integer: a total order with -0 < +0;
+//   amax    = max over |x| bit patterns: > inf's pattern iff some x is NaN.
+// The integer min/max are exactly associative, so every order gives the same
+// key; the paper's (a<b)*a + (a>=b)*b select is replaced by a
+// native integer min (IMNMX / redux.sync), which is branch-free and IEEE-safe.
+template <typename F, rd_op OP>
+struct FloatMinMax {
+  using T = F;
+  using U = typename std::conditional<sizeof(F) == 4, uint32_t, uint64_t>::type;
+  using S = typename std::conditional<sizeof(F) == 4, int32_t, int64_t>::type;
+  struct Acc { S key; U amax; };
+  static constexpr bool kFloat = true;
+  static constexpr U kAbsMask = (U)(~(U)0) >> 1;
+  static constexpr U kInfBits = sizeof(F) == 4 ? (U)0x7f800000u : (U)0x7ff0000000000000ull;
+
+  __device__ __forceinline__ static U bits(F x) {
+    if constexpr (sizeof(F) == 4) return __float_as_uint(x);
+    else return (U)__double_as_longlong(x);
+  }
+  __device__ __forceinline__ static S key_of(U b) { return (S)(b ^ ((U)((S)b >> (8 * sizeof(F) - 1)) & kAbsMask)); }
+  __device__ __forceinline__ static Acc identity() {
+    // min: key(+inf); max: key(-inf)
+    return OP == RD_MIN ? Acc{key_of(kInfBits), 0} : Acc{key_of(kInfBits | ~kAbsMask), 0};
+  }
+  __device__ __forceinline__ static S kmin(S a, S b) { return OP == RD_MIN ? (a < b ? a : b) : (a > b ? a : b); }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) {
+    return Acc{kmin(a.key, b.key), a.amax > b.amax ? a.amax : b.amax};
+  }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) {
+    U b = bits(x);
+    U m = b & kAbsMask;
+    return Acc{kmin(a.key, key_of(b)), a.amax > m ? a.amax : m};
+  }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+    if constexpr (sizeof(F) == 4) {
+      a.key = OP == RD_MIN ? __reduce_min_sync(0xffffffffu, (int)a.key) : __reduce_max_sync(0xffffffffu, (int)a.key);
+      a.amax = __reduce_max_sync(0xffffffffu, (unsigned)a.amax);
+      return a;
+    } else {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        Acc o{(S)shfl_xor_u64((uint64_t)a.key, m), (U)shfl_xor_u64((uint64_t)a.amax, m)};
+        a = combine(a, o);
+      }
+      return a;
+    }
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) {
+    U b = (a.amax > kInfBits) ? (kInfBits | ((U)1 << (sizeof(F) == 4 ? 22 : 51)))  // quiet NaN
+                              : (U)key_of((U)a.key);                              // key is an involution
+    *(U*)out = b;
+  }
+  __device__ __forceinline__ static void store_empty(void* out) {
+    *(U*)out = OP == RD_MIN ? kInfBits : (kInfBits | ~kAbsMask);
+  }
+  __device__ __forceinline__ static Slot pack(Acc a) { return Slot{(uint64_t)(U)a.key, (uint64_t)a.amax}; }
+  __device__ __forceinline__ static Acc unpack(Slot s) { return Acc{(S)(U)s.a, (U)s.b}; }
+};
+
+// ---------------------------------------------------------------- type map
+template <rd_dtype DT, rd_op OP> struct OpFor;
+#define RD_INT_OPS(DT, U, SIGNED)                                                  \
+  template <> struct OpFor<DT, RD_SUM> { using type = IntOp<U, RD_SUM, SIGNED>; }; \
+  template <> struct OpFor<DT, RD_PROD> { using type = IntOp<U, RD_PROD, SIGNED>; }; \
+  template <> struct OpFor<DT, RD_MIN> { using type = IntOp<U, RD_MIN, SIGNED>; }; \
+  template <> struct OpFor<DT, RD_MAX> { using type = IntOp<U, RD_MAX, SIGNED>; }; \
+  template <> struct OpFor<DT, RD_AND> { using type = IntOp<U, RD_AND, SIGNED>; }; \
+  template <> struct OpFor<DT, RD_OR> { using type = IntOp<U, RD_OR, SIGNED>; };   \
+  template <> struct OpFor<DT, RD_XOR> { using type = IntOp<U, RD_XOR, SIGNED>; };
+RD_INT_OPS(RD_INT32, uint32_t, true)
+RD_INT_OPS(RD_UINT32, uint32_t, false)
+RD_INT_OPS(RD_INT64, uint64_t, true)
+#undef RD_INT_OPS
+template <> struct OpFor<RD_FLOAT32, RD_SUM> { using type = FloatSum<float>; };
+template <> struct OpFor<RD_FLOAT64, RD_SUM> { using type = FloatSum<double>; };
+template <> struct OpFor<RD_FLOAT32, RD_PROD> { using type = Float32Prod; };
+template <> struct OpFor<RD_FLOAT64, RD_PROD> { using type = Float64Prod; };
+template <> struct OpFor<RD_FLOAT32, RD_MIN> { using type = FloatMinMax<float, RD_MIN>; };
+template <> struct OpFor<RD_FLOAT32, RD_MAX> { using type = FloatMinMax<float, RD_MAX>; };
+template <> struct OpFor<RD_FLOAT64, RD_MIN> { using type = FloatMinMax<double, RD_MIN>; };
+template <> struct OpFor<RD_FLOAT64, RD_MAX> { using type = FloatMinMax<double, RD_MAX>; };
+
+__host__ __device__ __forceinline__ constexpr uint32_t record_tag(int dtype, int op) {
+  return 0x52440000u | ((uint32_t)dtype << 8) | (uint32_t)op;
+}
+
+}  // namespace rd

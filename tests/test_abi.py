@@ -1,0 +1,120 @@
+"""The C-ABI library (CPU-only checks): it loads, exports every symbol that
+include/*.h declares, and its host-side logic (argument validation, identity
+table, shard split) behaves as the header states. No compute calls here."""
+import ctypes
+import glob
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1710_07358_b200 as rd
+from paper_1710_07358_b200 import _lib
+from paper_1710_07358_b200.build import build_library
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    build_library()
+
+
+def declared_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z_0-9]*\s*\*?\s+\*?([A-Za-z_][A-Za-z_0-9]*)\s*\(",
+                             src, flags=re.M):
+            names.add(m.group(1))
+    return names
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ["reduce", "reduce_partial", "reduce_multi", "rd_combine_records", "reduce_host",
+                 "rd_get_unique_id", "rd_comm_init", "rd_comm_destroy", "rd_comm_check",
+                 "rd_identity", "rd_release_workspaces", "rd_status_string", "rd_last_error",
+                 "rd_shard_range", "rd_reduce_ex"]:
+        assert must in names, must
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    for name in declared_functions():
+        assert hasattr(L, name), f"libb200reduce.so does not export {name}"
+    assert set(_lib.SIGNATURES) == declared_functions()
+
+
+def test_record_layout():
+    assert ctypes.sizeof(_lib.rd_record) == 32 == rd.RECORD_BYTES
+    assert ctypes.sizeof(_lib.rd_unique_id) == 128
+
+
+def test_status_strings():
+    L = _lib.lib()
+    for code, name in _lib.STATUS.items():
+        assert L.rd_status_string(code).decode() == name
+
+
+@pytest.mark.parametrize("dtype", ["int32", "uint32", "int64", "float32", "float64"])
+@pytest.mark.parametrize("op", list(rd.OPS))
+def test_identity_matches_oracle(dtype, op):
+    """Two independent implementations of the empty-result table agree."""
+    if dtype.startswith("float") and op in ("and", "or", "xor"):
+        with pytest.raises(rd.ReduceError) as e:
+            rd.identity(dtype, op)
+        assert e.value.status == 2
+        return
+    a = rd.identity(dtype, op)
+    b = oracle.identity(dtype, op)
+    assert a.tobytes() == b.tobytes()
+
+
+def test_validation_before_any_device_work():
+    """Bad calls fail synchronously with the documented status and touch nothing
+    (no CUDA device needed: validation precedes every CUDA call)."""
+    L = _lib.lib()
+    buf = (ctypes.c_char * 64)()
+    p = ctypes.addressof(buf)
+    p = p + (-p) % 16
+    out = ctypes.c_void_p(p)
+    assert L.reduce(None, 5, 0, 0, out, None) == 1                 # x NULL, n > 0
+    assert L.reduce(p, 5, 0, 0, None, None) == 1                   # out NULL
+    assert L.reduce(p, 5, 9, 0, out, None) == 1                    # unknown dtype
+    assert L.reduce(p, 5, 0, 9, out, None) == 1                    # unknown op
+    for op in (4, 5, 6):
+        assert L.reduce(p, 5, 3, op, out, None) == 2               # bitwise on float32
+        assert L.reduce(p, 5, 4, op, out, None) == 2               # bitwise on float64
+    assert L.reduce(p + 2, 5, 0, 0, out, None) == 3                # int32 base not 4-aligned
+    assert L.reduce(p + 4, 5, 2, 0, out, None) == 3                # int64 base not 8-aligned
+    assert L.reduce(p, 5, 2, 0, ctypes.c_void_p(p + 4), None) == 3  # out misaligned
+    assert L.reduce(p, 1 << 41, 0, 0, out, None) == 1              # n too large
+    assert "NULL" in L.rd_last_error().decode() or L.rd_last_error()
+    assert L.reduce_host(None, 3, 0, 0, out) == 1
+    assert L.rd_combine_records(None, 2, 0, 0, out, None, None, None) == 1
+    assert L.rd_combine_records(None, -1, 0, 0, out, None, None, None) == 1
+    assert L.reduce_multi(p, 4, 0, 0, out, None, None) == 1        # comm NULL
+    cfg = _lib.rd_config(7, 0, 0, 0, 0)
+    assert L.rd_reduce_ex(p, 4, 0, 0, out, None, ctypes.byref(cfg), None) == 1
+    cfg = _lib.rd_config(1, 32, 3, 0, 0)                           # U=3 only for the ablation pairs
+    assert L.rd_reduce_ex(p, 4, 2, 1, out, None, ctypes.byref(cfg), None) == 2
+
+
+@pytest.mark.parametrize("n", [0, 1, 7, 8, 1000, 5533214, (1 << 34) + 5])
+@pytest.mark.parametrize("W", [1, 2, 3, 4, 8])
+def test_shard_range_partitions(n, W):
+    """Contiguous blocks in rank order, covering [0, n) exactly, sizes differ by <= 1."""
+    spans = [rd.shard_range(n, W, r) for r in range(W)]
+    pos = 0
+    for b, c in spans:
+        assert b == pos
+        pos += c
+    assert pos == n
+    sizes = [c for _, c in spans]
+    assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(rd.ReduceError):
+        rd.shard_range(n, W, W)

@@ -1,0 +1,402 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element for
+element on the same seeded inputs. Needs a B200."""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+from tests import _brute, _parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+INT = ["int32", "uint32", "int64"]
+FLT = ["float32", "float64"]
+INT_OPS = ["sum", "prod", "min", "max", "and", "or", "xor"]
+FLT_OPS = ["sum", "prod", "min", "max"]
+PAIRS = [(d, o) for d in INT for o in INT_OPS] + [(d, o) for d in FLT for o in FLT_OPS]
+SIZES = [0, 1, 2, 3, 7, 8, 9, 31, 32, 33, 255, 256, 257, 1023, 1025, 4097, 65535, 65537,
+         (1 << 20) + 1, 5533214]
+
+
+@pytest.fixture(scope="module")
+def rd():
+    from paper_1710_07358_b200.build import build_all
+    build_all()
+    import paper_1710_07358_b200 as m
+    return m
+
+
+def to_dev(x: np.ndarray, offset: int = 0):
+    """Copy x to the GPU at an element offset from a 512-byte-aligned allocation."""
+    dt = getattr(torch, x.dtype.name)
+    carrier = {4: np.int32, 8: np.int64}[x.dtype.itemsize]
+    buf = torch.empty(x.size + offset + 1, dtype=getattr(torch, np.dtype(carrier).name), device="cuda")
+    if x.size:
+        buf[offset:offset + x.size].copy_(torch.from_numpy(x.view(carrier)))
+    return buf.view(dt)[offset:offset + x.size]
+
+
+def val(t):
+    """0-d CUDA tensor -> numpy scalar of the same dtype (bit-preserving)."""
+    carrier = {4: torch.int32, 8: torch.int64}[t.element_size()]
+    npdt = np.dtype(str(t.dtype).replace("torch.", ""))
+    return np.array([t.view(carrier).item()], dtype=np.dtype(str(carrier).replace("torch.", ""))).view(npdt)[0]
+
+
+# ------------------------------------------------------------------ C1
+def test_c1_iota_int32_closed_form(rd):
+    """BASELINE configs[0]: int32 sum of iota, n = 2^20 -> -524288 (= n(n-1)/2 mod 2^32)."""
+    n = 1 << 20
+    x = torch.empty(n, dtype=torch.int32, device="cuda")
+    inputs.fill_device(x, "iota")
+    assert int(val(rd.reduce(x, "sum"))) == -524288
+    for seed in (1, 2, 3):
+        xh = inputs.generate(n, "int32", "uniform_bits", seed=seed)
+        _parity.check(val(rd.reduce(to_dev(xh), "sum")), xh, "sum")
+
+
+# ------------------------------------------------------------------ C3/C4 matrix
+@pytest.mark.parametrize("dtype,op", PAIRS, ids=[f"{d}-{o}" for d, o in PAIRS])
+def test_matrix_sizes(rd, dtype, op):
+    wl = inputs.default_workload(dtype, op)
+    for n in SIZES:
+        x = inputs.generate(n, dtype, wl, seed=n % 7 + 1)
+        _parity.check(val(rd.reduce(to_dev(x), op)), x, op)
+
+
+@pytest.mark.parametrize("dtype,op", PAIRS, ids=[f"{d}-{o}" for d, o in PAIRS])
+def test_misaligned_bases(rd, dtype, op):
+    """C4: element offsets 0..7 from an aligned allocation (head + body + tail)."""
+    wl = inputs.default_workload(dtype, op)
+    for n in (5, 13, 1000, 100003):
+        x = inputs.generate(n, dtype, wl, seed=11)
+        for off in range(8):
+            _parity.check(val(rd.reduce(to_dev(x, off), op)), x, op)
+
+
+@pytest.mark.parametrize("dtype,op", [("float32", "sum"), ("int64", "prod"), ("float64", "max"),
+                                      ("uint32", "min"), ("float64", "prod"), ("int32", "xor")])
+def test_forced_grids(rd, dtype, op):
+    """a6 ticket combine for any grid size, including 1 (no ticket) and the cap."""
+    wl = inputs.default_workload(dtype, op)
+    x = inputs.generate((1 << 20) + 5, dtype, wl, seed=5)
+    xd = to_dev(x, 3)
+    for g in (1, 2, 3, 7, 148, 593, 1000, 4096):
+        out, info = rd.reduce_ex(xd, op, grid=g)
+        assert info["grid"] == g
+        _parity.check(val(out), x, op)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "int32"])
+def test_ablation_configs(rd, dtype):
+    """Every compiled configuration of the loads-in-flight sweep (Table 2 on B200)."""
+    wl = "u01" if dtype == "float32" else "uniform_bits"
+    x = inputs.generate(5533214, dtype, wl, seed=2)
+    for off in (0, 1):
+        xd = to_dev(x, off)
+        for vb in (4, 8, 16, 32):
+            for u in (1, 2, 3, 4, 5, 6, 7, 8, 16):
+                out, info = rd.reduce_ex(xd, "sum", variant="vector", unroll=u, vec_bytes=vb)
+                assert (info["unroll"], info["vec_bytes"]) == (u, vb)
+                _parity.check(val(out), x, "sum")
+        for f in (1, 2, 3, 4, 5, 6, 7, 8, 16):
+            out, info = rd.reduce_ex(xd, "sum", variant="paper", unroll=f)
+            assert info["variant"] == "paper" and info["unroll"] == f
+            _parity.check(val(out), x, "sum")
+
+
+# ------------------------------------------------------------------ special values
+@pytest.mark.parametrize("prec", FLT)
+def test_absorption_example(rd, prec):
+    """P:50 fn 2: 1.5 + 4^50 - 4^50 is 0 or 1.5 depending on the order; the GPU
+    returns one of the tree results for every ordering and alignment."""
+    big = 4.0 ** 50
+    for order in ([1.5, big, -big], [big, -big, 1.5], [big, 1.5, -big]):
+        x = np.array(order, dtype=prec)
+        for off in range(4):
+            g = float(val(rd.reduce(to_dev(x, off), "sum")))
+            assert g in {0.0, 1.5}
+            _parity.check(g, x, "sum")
+
+
+@pytest.mark.parametrize("prec", FLT)
+def test_small_n_float_sum_is_a_tree_result(rd, prec):
+    """n <= 8: several results are correct (every evaluation tree); the
+    GPU's must be one of them (set membership by brute force)."""
+    rng = np.random.default_rng(1)
+    for n in range(1, 9):
+        for trial in range(8):
+            x = (rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, n)).astype(prec)
+            trees = _brute.tree_results(list(x), "sum", prec)
+            for off in (0, 3):
+                g = float(val(rd.reduce(to_dev(x, off), "sum")))
+                assert g in trees, (n, trial, off)
+
+
+@pytest.mark.parametrize("prec", FLT)
+def test_minmax_special_values(rd, prec):
+    """IEEE minimum/maximum (NaN propagates, -0 < +0), bit-exact, in head, body and tail."""
+    dom = [0.0, -0.0, 1.0, -1.0, math.inf, -math.inf, math.nan, 1e-45, -2.5]
+    import itertools
+    for k in (1, 2, 3):
+        for combo in itertools.product(dom, repeat=k):
+            x = np.array(combo, dtype=prec)
+            for op in ("min", "max"):
+                _parity.check(val(rd.reduce(to_dev(x, 1), op)), x, op)
+    rng = np.random.default_rng(3)
+    base = inputs.generate(100000, prec, "u01", seed=3) + 1
+    for v in dom:
+        for pos in (0, 5, 777, 50000, 99999):
+            x = base.copy()
+            x[pos] = v
+            x[rng.integers(0, x.size)] = -0.0 if v == 0.0 else x[0]
+            for op in ("min", "max"):
+                _parity.check(val(rd.reduce(to_dev(x, pos % 8), op)), x, op)
+
+
+@pytest.mark.parametrize("prec", FLT)
+def test_signed_zero_and_nonfinite_sums(rd, prec):
+    """Padding uses -0.0 (the additive identity): an all -0.0 input sums to -0.0
+    at every size; empty input gives +0.0; inf/NaN classes follow IEEE."""
+    for n in (1, 2, 9, 100, 4099, 1 << 20):
+        x = np.full(n, -0.0, dtype=prec)
+        g = val(rd.reduce(to_dev(x, n % 5), "sum"))
+        assert _parity.to_bits(g, prec) == _parity.to_bits(-0.0, prec)
+    g = val(rd.reduce(to_dev(np.zeros(0, prec)), "sum"))
+    assert _parity.to_bits(g, prec) == _parity.to_bits(0.0, prec)
+    # near-one data: no partial product under/overflows in any order, so the
+    # class of the result (inf / NaN) is order-independent
+    base = inputs.generate(10000, prec, "near_one", seed=4)
+    for a, b in [(math.inf, 1.0), (math.inf, -math.inf), (math.nan, 0.0), (-math.inf, 2.0)]:
+        x = base.copy()
+        x[17], x[9000] = a, b
+        for op in ("sum", "prod"):
+            _parity.check(val(rd.reduce(to_dev(x, 2), op)), x, op)
+    x = base.copy()
+    x[123] = 0.0
+    _parity.check(val(rd.reduce(to_dev(x), "prod")), x, "prod")
+
+
+@pytest.mark.parametrize("dtype", INT)
+def test_integer_wraparound(rd, dtype):
+    """+ and x wrap mod 2^w; min/max respect signedness (values near the extremes)."""
+    info = np.iinfo(dtype)
+    x = np.array([info.max, 1, info.max, info.min, 3, -1 if dtype != "uint32" else 7] * 1001,
+                 dtype=dtype)
+    for op in INT_OPS:
+        _parity.check(val(rd.reduce(to_dev(x, 1), op)), x, op)
+
+
+# ------------------------------------------------------------------ generator twin
+@pytest.mark.parametrize("dtype", INT + FLT)
+def test_device_generator_matches_host(rd, dtype):
+    for wl in inputs.WORKLOADS:
+        try:
+            h = inputs.generate(100003, dtype, wl, seed=9, offset=12345, n_total=10 ** 7)
+        except ValueError:
+            continue
+        d = torch.empty(100003, dtype=getattr(torch, dtype), device="cuda")
+        inputs.fill_device(d, wl, seed=9, offset=12345, n_total=10 ** 7)
+        assert d.cpu().numpy().tobytes() == h.tobytes(), wl
+
+
+# ------------------------------------------------------------------ determinism, graphs, streams
+def test_determinism(rd):
+    x = torch.empty(1 << 24, dtype=torch.float32, device="cuda")
+    inputs.fill_device(x, "normalish", seed=2)
+    a = [val(rd.reduce(x, "sum")).tobytes() for _ in range(5)]
+    assert len(set(a)) == 1
+
+
+def test_cuda_graph_capture(rd):
+    n = (1 << 22) + 3
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    inputs.fill_device(x, "u01", seed=5)
+    s = torch.cuda.Stream()
+    out = torch.empty((), dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(s):
+        rd.reduce(x, "sum", out=out)            # creates the stream's workspace outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        rd.reduce(x, "sum", out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    _parity.check(val(out), x.cpu().numpy(), "sum")
+
+
+def test_concurrent_streams(rd):
+    """Separate per-stream workspaces: concurrent reductions do not interfere."""
+    xs = [inputs.generate((1 << 21) + i, "int64", "uniform_bits", seed=i) for i in range(4)]
+    ds = [to_dev(x) for x in xs]
+    streams = [torch.cuda.Stream() for _ in xs]
+    outs = []
+    for rep in range(3):
+        outs = []
+        for d, s in zip(ds, streams):
+            with torch.cuda.stream(s):
+                outs.append(rd.reduce(d, "sum"))
+        torch.cuda.synchronize()
+        for o, x in zip(outs, xs):
+            _parity.check(val(o), x, "sum")
+
+
+# ------------------------------------------------------------------ records / sharding
+@pytest.mark.parametrize("dtype,op", [("float32", "sum"), ("float64", "sum"), ("int64", "prod"),
+                                      ("float64", "prod"), ("float32", "max"), ("uint32", "and"),
+                                      ("int32", "min"), ("float32", "prod")])
+def test_shard_records_combine(rd, dtype, op):
+    """Split one logical array into W contiguous shards (rd_shard_range), reduce
+    each to a record, fold the records in rank order: parity with the oracle on
+    the whole array (the exchange step of reduce_multi, without the transport)."""
+    n = (1 << 22) + 3
+    wl = inputs.default_workload(dtype, op)
+    x = inputs.generate(n, dtype, wl, seed=7)
+    xd = to_dev(x)
+    for W in (1, 2, 3, 8, 17):
+        recs = torch.empty(W * 32, dtype=torch.uint8, device="cuda")
+        for r in range(W):
+            b, c = rd.shard_range(n, W, r)
+            rd.reduce_partial(xd[b:b + c], op, rec=recs[r * 32:(r + 1) * 32])
+        out = rd.combine_records(recs, dtype, op)
+        _parity.check(val(out), x, op)
+
+
+def test_record_mismatch_detected(rd):
+    x = to_dev(inputs.generate(1000, "float32", "u01"))
+    recs = torch.empty(64, dtype=torch.uint8, device="cuda")
+    rd.reduce_partial(x, "sum", rec=recs[:32])
+    rd.reduce_partial(x, "max", rec=recs[32:])
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = rd.combine_records(recs, "float32", "sum", status=status)
+    assert int(status.item()) == 6
+    assert float(val(out)) == 0.0
+
+
+def test_empty_shards(rd):
+    recs = torch.empty(3 * 32, dtype=torch.uint8, device="cuda")
+    x = inputs.generate(100, "float32", "u01")
+    xd = to_dev(x)
+    rd.reduce_partial(xd[:0], "sum", rec=recs[0:32])
+    rd.reduce_partial(xd, "sum", rec=recs[32:64])
+    rd.reduce_partial(xd[:0], "sum", rec=recs[64:96])
+    _parity.check(val(rd.combine_records(recs, "float32", "sum")), x, "sum")
+
+
+# ------------------------------------------------------------------ host entry point
+@pytest.mark.parametrize("dtype,op", [("float32", "sum"), ("int32", "xor"), ("float64", "prod"),
+                                      ("int64", "max"), ("uint32", "sum")])
+def test_reduce_host(rd, dtype, op):
+    n = (1 << 25) + 7   # several 32 MiB chunks
+    wl = inputs.default_workload(dtype, op)
+    x = inputs.generate(n, dtype, wl, seed=3)
+    _parity.check(rd.reduce_host(x, op), x, op)                 # pageable
+    pinned = torch.from_numpy(x.view({4: np.int32, 8: np.int64}[x.itemsize])).pin_memory()
+    pinned = pinned.view(getattr(torch, dtype))
+    _parity.check(rd.reduce_host(pinned, op), x, op)            # pinned
+    for m in (0, 1, 5):
+        _parity.check(rd.reduce_host(x[:m], op), x[:m], op)
+
+
+# ------------------------------------------------------------------ NCCL path (1 rank)
+def test_reduce_multi_single_rank(rd):
+    from paper_1710_07358_b200 import _lib
+    L = _lib.lib()
+    uid = _lib.rd_unique_id()
+    assert L.rd_get_unique_id(ctypes.byref(uid)) == 0
+    h = ctypes.c_void_p()
+    assert L.rd_comm_init(ctypes.byref(h), 1, 0, ctypes.byref(uid), torch.cuda.current_device()) == 0
+    comm = rd.Comm(h.value, 1, 0, torch.cuda.current_device())
+    try:
+        for dtype, op in [("float32", "sum"), ("int32", "xor"), ("float64", "min")]:
+            x = inputs.generate((1 << 20) + 9, dtype, inputs.default_workload(dtype, op), seed=1)
+            _parity.check(val(comm.reduce(to_dev(x, 1), op)), x, op)
+        comm.check()
+    finally:
+        comm.destroy()
+
+
+# ------------------------------------------------------------------ full BASELINE sizes
+def _device_input(n, dtype, wl, seed):
+    x = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
+    inputs.fill_device(x, wl, seed=seed)
+    return x
+
+
+@pytest.mark.parametrize("dtype", FLT)
+@pytest.mark.parametrize("wl", ["u01", "normalish"])
+def test_c2_full_size(rd, dtype, wl):
+    """BASELINE configs[1]: float32 / float64 sum, n = 2^28, seeds 1-3, vs the fp64 oracle."""
+    n = 1 << 28
+    for seed in (1, 2, 3):
+        x = _device_input(n, dtype, wl, seed)
+        g = val(rd.reduce(x, "sum"))
+        xh = x.cpu().numpy()
+        del x
+        _parity.check(g, xh, "sum")
+
+
+def test_c2_exact_variants(rd):
+    """Inputs whose sum is exact in any order: the GPU must return it bit-exactly."""
+    n = 1 << 28
+    x = _device_input(n, "float64", "int_small", 1)
+    xi = _device_input(n, "int64", "int_small", 1)
+    assert float(val(rd.reduce(x, "sum"))) == float(int(val(rd.reduce(xi, "sum"))))
+    del x, xi
+    x = _device_input(n, "float32", "sparse_pm1", 2)
+    xi = _device_input(n, "int32", "sparse_pm1", 2)
+    assert float(val(rd.reduce(x, "sum"))) == float(int(val(rd.reduce(xi, "sum"))))
+    for prec in FLT:
+        x = _device_input(n, prec, "pow2_sparse", 3)
+        e = int((x == 2).sum().item()) - int((x == 0.5).sum().item())
+        assert float(val(rd.reduce(x, "prod"))) == 2.0 ** e
+
+
+@pytest.mark.parametrize("dtype", INT)
+def test_closed_forms_2_30(rd, dtype):
+    """iota at n = 2^30 (4-8 GiB): n(n-1)/2 mod 2^w, xor closed form, min/max."""
+    n = 1 << 30
+    x = _device_input(n, dtype, "iota", 1)
+    w = 64 if dtype == "int64" else 32
+    s = (n * (n - 1) // 2) % (1 << w)
+    assert int(val(rd.reduce(x, "sum"))) & ((1 << w) - 1) == s
+    assert int(val(rd.reduce(x, "xor"))) == [n - 1, 1, n, 0][(n - 1) % 4]
+    assert int(val(rd.reduce(x, "min"))) == 0
+    assert int(val(rd.reduce(x, "max"))) == n - 1
+
+
+@pytest.mark.parametrize("dtype,op", [("float32", "sum"), ("int32", "sum"), ("float32", "max"),
+                                      ("int32", "prod")])
+def test_c3_2_30_vs_oracle(rd, dtype, op):
+    """C3's largest size, n = 2^30, against the oracle on the whole array."""
+    n = 1 << 30
+    x = _device_input(n, dtype, inputs.default_workload(dtype, op), 1)
+    g = val(rd.reduce(x, op))
+    xh = x.cpu().numpy()
+    del x
+    _parity.check(g, xh, op)
+
+
+def test_c5_sharded_layout_on_one_gpu(rd):
+    """BASELINE configs[4] layout (float32 sum and max, sharded over W = 8 ranks)
+    at n = 2^30 on one GPU: shard records folded in rank order == oracle."""
+    n, W = 1 << 30, 8
+    for op, wl in (("sum", "u01"), ("max", "planted")):
+        x = _device_input(n, "float32", wl, 1)
+        recs = torch.empty(W * 32, dtype=torch.uint8, device="cuda")
+        for r in range(W):
+            b, c = rd.shard_range(n, W, r)
+            rd.reduce_partial(x[b:b + c], op, rec=recs[r * 32:(r + 1) * 32])
+        g = val(rd.combine_records(recs, "float32", op))
+        xh = x.cpu().numpy()
+        del x
+        _parity.check(g, xh, op)
+        if op == "max":
+            assert float(g) == 2.0 ** 20
