@@ -172,13 +172,17 @@ const char* rd_last_error(void);
  *   variant   RD_VARIANT_AUTO, RD_VARIANT_VECTOR (grid-stride vector loads),
  *             RD_VARIANT_PAPER (PAPER.md Listing "Unrolling the step 1",
  *             F consecutive elements per work-item per iteration,
- *             bounds handled by predication instead of the (i<len)*x mask)
- *   vec_bytes 4, 8, 16 or 32 bytes per load (VECTOR variant)
- *   unroll    loads in flight per thread per iteration (U; the paper's F)
+ *             bounds handled by predication instead of the (i<len)*x mask),
+ *             RD_VARIANT_BULK (cp.async.bulk shared-memory ring, dynamic
+ *             chunk scheduling, per-chunk partials: still deterministic)
+ *   vec_bytes 4, 8, 16 or 32 bytes per load (VECTOR variant);
+ *             bytes per ring stage (BULK variant)
+ *   unroll    loads in flight per thread per iteration (U; the paper's F);
+ *             ring stages (BULK variant)
  *   grid      CTAs (clamped to [1, 4096])
  * The chosen configuration is written to *info (may be NULL).
  * Configurations without a compiled kernel return RD_ERR_UNSUPPORTED. */
-enum { RD_VARIANT_AUTO = 0, RD_VARIANT_VECTOR = 1, RD_VARIANT_PAPER = 2 };
+enum { RD_VARIANT_AUTO = 0, RD_VARIANT_VECTOR = 1, RD_VARIANT_PAPER = 2, RD_VARIANT_BULK = 3 };
 typedef struct { int32_t variant, vec_bytes, unroll, block, grid, reserved[3]; } rd_config;
 typedef struct {
   int32_t variant, vec_bytes, unroll, block, grid, regs_per_thread, ctas_per_sm, reserved;

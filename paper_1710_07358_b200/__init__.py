@@ -30,7 +30,8 @@ OPS = {"sum": _lib.RD_SUM, "prod": _lib.RD_PROD, "min": _lib.RD_MIN, "max": _lib
 DTYPE_NAMES = {"int32": _lib.RD_INT32, "uint32": _lib.RD_UINT32, "int64": _lib.RD_INT64,
                "float32": _lib.RD_FLOAT32, "float64": _lib.RD_FLOAT64}
 RECORD_BYTES = 32
-VARIANTS = {"auto": _lib.RD_VARIANT_AUTO, "vector": _lib.RD_VARIANT_VECTOR, "paper": _lib.RD_VARIANT_PAPER}
+VARIANTS = {"auto": _lib.RD_VARIANT_AUTO, "vector": _lib.RD_VARIANT_VECTOR, "paper": _lib.RD_VARIANT_PAPER,
+            "bulk": _lib.RD_VARIANT_BULK}
 
 
 def _torch():

@@ -16,7 +16,7 @@ RD_SUM, RD_PROD, RD_MIN, RD_MAX, RD_AND, RD_OR, RD_XOR = range(7)
 RD_OK = 0
 STATUS = {0: "RD_OK", 1: "RD_ERR_INVALID_ARG", 2: "RD_ERR_UNSUPPORTED", 3: "RD_ERR_MISALIGNED",
           4: "RD_ERR_CUDA", 5: "RD_ERR_NCCL", 6: "RD_ERR_MISMATCH"}
-RD_VARIANT_AUTO, RD_VARIANT_VECTOR, RD_VARIANT_PAPER = 0, 1, 2
+RD_VARIANT_AUTO, RD_VARIANT_VECTOR, RD_VARIANT_PAPER, RD_VARIANT_BULK = 0, 1, 2, 3
 
 
 class rd_record(ctypes.Structure):

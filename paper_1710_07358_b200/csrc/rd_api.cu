@@ -42,8 +42,9 @@ rd_status check_dtype_op(int dtype, int op) {
 namespace {
 
 struct Workspace {
-  Slot* partials = nullptr;   // kMaxGrid slots
-  unsigned* ticket = nullptr; // one counter, zero between launches
+  Slot* partials = nullptr;   // kMaxGrid slots (per CTA, or per chunk for the bulk variant)
+  unsigned* ticket = nullptr; // CTAs finished, zero between launches
+  unsigned* work = nullptr;   // bulk variant: next chunk, zero between launches
 };
 
 struct DeviceInfo {
@@ -75,6 +76,7 @@ rd_status get_workspace(int dev, cudaStream_t stream, Workspace* out) {
   if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "workspace init"); }
   w.partials = (Slot*)p;
   w.ticket = (unsigned*)((char*)p + sizeof(Slot) * kMaxGrid);
+  w.work = w.ticket + 32;     // separate 128-byte line
   g_ws[key] = w;
   *out = w;
   return RD_OK;
@@ -98,7 +100,12 @@ rd_status occupancy(int dev, const KernelRef& k, int* ctas, int* regs) {
   auto it = g_occ.find(key);
   if (it != g_occ.end()) { *ctas = it->second; *regs = g_regs[key]; return RD_OK; }
   int c = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k.fn, k.block, 0);
+  cudaError_t e = cudaSuccess;
+  if (k.smem_bytes > 48 * 1024) {
+    e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k.fn, k.block, k.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   cudaFuncAttributes fa;
   e = cudaFuncGetAttributes(&fa, k.fn);
@@ -134,19 +141,22 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   if (mode == 1 && (uintptr_t)rec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
 
-  const int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
+  int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
   const int unroll = cfg ? cfg->unroll : 0;
   const int vec_bytes = cfg ? cfg->vec_bytes : 0;
-  if (cfg && (cfg->block != 0 && cfg->block != kBlock)) {
-    set_error("only block = 256 is compiled");
+  if (cfg && cfg->block != 0 && !((cfg->block == kBlock && variant != RD_VARIANT_BULK) ||
+                                   (cfg->block == 32 * (kBulkConsumerWarps + 1) && variant == RD_VARIANT_BULK))) {
+    set_error("block size not compiled for this variant");
     return RD_ERR_UNSUPPORTED;
   }
-  if (variant < RD_VARIANT_AUTO || variant > RD_VARIANT_PAPER || unroll < 0 || vec_bytes < 0 ||
+  if (variant < RD_VARIANT_AUTO || variant > RD_VARIANT_BULK || unroll < 0 || vec_bytes < 0 ||
       (cfg && cfg->grid < 0)) {
     set_error("bad rd_config");
     return RD_ERR_INVALID_ARG;
   }
-  if (vec_bytes && vec_bytes < s) { set_error("vec_bytes < sizeof(dtype)"); return RD_ERR_INVALID_ARG; }
+  if (vec_bytes && vec_bytes < s && variant != RD_VARIANT_BULK) { set_error("vec_bytes < sizeof(dtype)"); return RD_ERR_INVALID_ARG; }
+  if (variant == RD_VARIANT_AUTO && unroll == 0 && vec_bytes == 0 && (uint64_t)n * s >= kBulkMinBytes)
+    variant = RD_VARIANT_BULK;   // planner: large inputs take the bulk-copy pipeline
   KernelRef k;
   if (!lookup(dtype, op, variant, unroll, vec_bytes, &k)) {
     set_error("no compiled kernel for this (dtype, op, variant, unroll, vec_bytes)");
@@ -164,34 +174,46 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   if ((st = get_workspace(dev, stream, &ws)) != RD_OK) return st;
 
   KArgs a;
+  std::memset(&a, 0, sizeof(a));
   a.x = (const unsigned char*)x;
   a.n = n;
-  uint64_t units;  // work units handed out by the grid-stride loop
-  if (k.variant == RD_VARIANT_VECTOR) {
-    const uint64_t L = (uint64_t)(k.vec_bytes / s);
-    const uint64_t mis = (uint64_t)((uintptr_t)x % (uintptr_t)k.vec_bytes);
-    uint64_t head = ((k.vec_bytes - mis) % k.vec_bytes) / s;
+  uint64_t g = (uint64_t)di.sms * occ;   // persistent grid
+  if (k.variant == RD_VARIANT_VECTOR || k.variant == RD_VARIANT_BULK) {
+    const int vb = k.variant == RD_VARIANT_BULK ? 16 : k.vec_bytes;   // body alignment
+    const uint64_t L = (uint64_t)(vb / s);
+    const uint64_t mis = (uint64_t)((uintptr_t)x % (uintptr_t)vb);
+    uint64_t head = ((vb - mis) % vb) / s;
     if (head > n) head = n;
     a.head = head;
     a.nvec = (n - head) / L;
     a.tail_start = head + a.nvec * L;
     a.tail = n - a.tail_start;
-    units = a.nvec;
   } else {  // PAPER: F consecutive elements per work-item
     a.head = 0;
     a.nvec = 0;
     a.tail_start = n;
     a.tail = 0;
-    units = (n + k.unroll - 1) / k.unroll;
-    k.unroll = k.unroll;
   }
-  // Persistent grid: at most the CTAs that are resident
-  // at once, fewer when there is less work than one unrolled pass.
-  const uint64_t per_cta = (uint64_t)k.block * (k.variant == RD_VARIANT_VECTOR ? k.unroll : 1);
-  uint64_t g = (uint64_t)di.sms * occ;
-  uint64_t need = (units + per_cta - 1) / per_cta;
-  if (need < 1) need = 1;
-  if (g > need) g = need;
+  if (k.variant == RD_VARIANT_BULK) {
+    // chunks of whole stages, at most kMaxGrid of them; fixed by n and alignment only
+    const uint64_t body_bytes = a.nvec * 16;
+    const uint64_t stage = (uint64_t)k.vec_bytes;
+    uint64_t stages_per_chunk = (body_bytes + stage * kMaxGrid - 1) / (stage * kMaxGrid);
+    if (stages_per_chunk < 4) stages_per_chunk = 4;
+    a.chunk_bytes = stages_per_chunk * stage;
+    a.nchunks = (uint32_t)((body_bytes + a.chunk_bytes - 1) / a.chunk_bytes);
+    a.work = ws.work;
+    uint64_t need = a.nchunks ? a.nchunks : 1;
+    if (g > need) g = need;
+  } else {
+    // work units handed out by the grid-stride loop; fewer CTAs than one
+    // resident wave when there is less work than one unrolled pass
+    const uint64_t units = k.variant == RD_VARIANT_VECTOR ? a.nvec : (n + k.unroll - 1) / k.unroll;
+    const uint64_t per_cta = (uint64_t)k.block * (k.variant == RD_VARIANT_VECTOR ? k.unroll : 1);
+    uint64_t need = (units + per_cta - 1) / per_cta;
+    if (need < 1) need = 1;
+    if (g > need) g = need;
+  }
   if (cfg && cfg->grid > 0) g = (uint64_t)cfg->grid;
   if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
   if (g < 1) g = 1;
@@ -203,7 +225,7 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   a.tag = record_tag(dtype, op);
   a.mode = mode;
 
-  k.fn<<<(unsigned)g, k.block, 0, stream>>>(a);
+  k.fn<<<(unsigned)g, k.block, k.smem_bytes, stream>>>(a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
   if (info) {

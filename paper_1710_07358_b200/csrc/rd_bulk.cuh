@@ -1,0 +1,231 @@
+// rd_bulk.cuh -- the bulk-copy pipeline variant of Step 1 (the
+// "optional TMA or cp.async.bulk shared-memory staging pipeline" of the north
+// star).
+//
+// One persistent CTA per SM = 1 producer warp + CW consumer warps.
+//  producer (one elected lane): takes the next CHUNK of the 16-byte-aligned
+//    body from a global counter (dynamic scheduling: faster SMs take more
+//    chunks, which removes the static partition's tail), and streams it into
+//    a STAGES-deep shared-memory ring with cp.async.bulk (UBLKCP), one
+//    mbarrier per stage carrying the transaction bytes.
+//  consumers: wait on the stage's mbarrier, LDS.128 their fixed slice of the
+//    stage, fold into lane accumulators, release the stage. At the end of a
+//    chunk the CTA reduces the chunk to ONE partial, stored at
+//    partials[chunk] -- so the result does not depend on which CTA took which
+//    chunk: the reduction tree is fixed by n and the base alignment alone
+//    (deterministic, like the vector variant).
+//  last CTA (atomic ticket): folds partials[0..nchunks) in chunk order plus
+//    the head/tail stragglers, writes the result, resets ticket and counter.
+// In-flight bytes per SM are STAGES * STAGE_BYTES of shared memory (up to
+// 192 KB) instead of registers.
+#pragma once
+#include "rd_kernels.cuh"
+
+namespace rd {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "RD_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra RD_WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+template <int STAGES, int STAGE_BYTES, int CW>
+struct BulkSmem {
+  static constexpr int kRing = STAGES * STAGE_BYTES;
+  static constexpr int kBytes = kRing + 1024;   // ring + barriers + stage metadata + partials
+};
+
+template <class OpT, int STAGES, int STAGE_BYTES, int CW>
+__global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs args) {
+  using T = typename OpT::T;
+  using Acc = typename OpT::Acc;
+  constexpr int CT = 32 * CW;                          // consumer threads
+  constexpr int L = 16 / (int)sizeof(T);               // lanes per 16-byte vector
+  constexpr int PER_THREAD = STAGE_BYTES / (16 * CT);  // LDS.128 per thread per stage
+  static_assert(STAGE_BYTES % (16 * CT) == 0, "stage must split evenly over consumer threads");
+  constexpr int B = 32 * (CW + 1);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* ring = smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  int32_t* st_chunk = reinterpret_cast<int32_t*>(empty + STAGES);
+  uint32_t* st_bytes = reinterpret_cast<uint32_t*>(st_chunk + STAGES);
+  uint32_t* st_last = st_bytes + STAGES;
+  Acc* wpart = reinterpret_cast<Acc*>(reinterpret_cast<uintptr_t>(st_last + STAGES + 3) & ~(uintptr_t)15);  // [2][CW]
+  __shared__ Acc red[32];
+
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const unsigned char* body = args.x + args.head * sizeof(T);
+  const uint64_t body_bytes = args.nvec * 16;
+
+  if (warp == CW) {
+    // ---------------------------------------------------------------- producer
+    if (ln == 0) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (;;) {
+        const uint32_t c = atomicAdd(args.work, 1u);
+        if (c >= args.nchunks) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          st_chunk[stage] = -1;
+          mbar_arrive(&full[stage]);
+          break;
+        }
+        const uint64_t cbeg = (uint64_t)c * args.chunk_bytes;
+        const uint64_t cend = min(cbeg + args.chunk_bytes, body_bytes);
+        for (uint64_t off = cbeg; off < cend; off += STAGE_BYTES) {
+          const uint32_t bytes = (uint32_t)min((uint64_t)STAGE_BYTES, cend - off);
+          mbar_wait(&empty[stage], phase ^ 1);
+          st_chunk[stage] = (int32_t)c;
+          st_bytes[stage] = bytes;
+          st_last[stage] = (off + bytes == cend);
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(ring + (size_t)stage * STAGE_BYTES, body + off, bytes, &full[stage], pol);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- consumers
+    const int t = threadIdx.x;  // 0 .. CT-1
+    Acc acc[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) acc[l] = OpT::identity();
+    int stage = 0;
+    uint32_t phase = 0, nchunk_local = 0;
+    const uint32_t ring_addr = smem_addr(ring);
+    for (;;) {
+      mbar_wait(&full[stage], phase);
+      const int32_t c = st_chunk[stage];
+      if (c < 0) break;
+      const uint32_t bytes = st_bytes[stage];
+      const uint32_t last = st_last[stage];
+      const uint32_t base = ring_addr + stage * STAGE_BYTES;
+      if (bytes == STAGE_BYTES) {
+        uint4 v[PER_THREAD];
+#pragma unroll
+        for (int k = 0; k < PER_THREAD; ++k) v[k] = lds128(base + (k * CT + t) * 16);
+#pragma unroll
+        for (int k = 0; k < PER_THREAD; ++k) {
+          Vec<16> w{{v[k].x, v[k].y, v[k].z, v[k].w}};
+#pragma unroll
+          for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, 16>(w, l));
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < PER_THREAD; ++k) {
+          const uint32_t off = (k * CT + t) * 16;
+          if (off < bytes) {
+            uint4 q = lds128(base + off);
+            Vec<16> w{{q.x, q.y, q.z, q.w}};
+#pragma unroll
+            for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, 16>(w, l));
+          }
+        }
+      }
+      __syncwarp();
+      if (ln == 0) mbar_arrive(&empty[stage]);
+      if (last) {
+        // the chunk's partial: fixed tree over (thread, lane) -> independent of the schedule
+        Acc a = acc[0];
+#pragma unroll
+        for (int l = 1; l < L; ++l) a = OpT::combine(a, acc[l]);
+        a = OpT::warp_reduce(a);
+        Acc* wp = wpart + (nchunk_local & 1) * CW;
+        if (ln == 0) wp[warp] = a;
+        named_sync(1, CT);
+        if (warp == 0) {
+          Acc b = (ln < CW) ? wp[ln] : OpT::identity();
+          b = OpT::warp_reduce(b);
+          if (ln == 0) {
+            Slot s = OpT::pack(b);
+            __stcg(reinterpret_cast<ulonglong2*>(args.partials + c), make_ulonglong2(s.a, s.b));
+          }
+        }
+        ++nchunk_local;
+#pragma unroll
+        for (int l = 0; l < L; ++l) acc[l] = OpT::identity();
+      }
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+  }
+  // ------------------------------------------------------------------ grid combine
+  __syncthreads();
+  __shared__ unsigned s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();                                   // release this CTA's chunk partials
+    const unsigned tk = atomicAdd(args.ticket, 1u);
+    s_last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  Acc b = OpT::identity();
+  for (uint32_t j = threadIdx.x; j < args.nchunks; j += B) {
+    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(args.partials + j));
+    b = OpT::combine(b, OpT::unpack(Slot{v.x, v.y}));
+  }
+  if (threadIdx.x < args.head) b = OpT::fold(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)));
+  if (threadIdx.x < args.tail)
+    b = OpT::fold(b, ldg_scalar<T>(args.x + (args.tail_start + threadIdx.x) * sizeof(T)));
+  b = block_reduce<OpT, B>(b, red);
+  if (threadIdx.x == 0) {
+    finish<OpT>(b, args);
+    *args.ticket = 0u;
+    *args.work = 0u;
+  }
+}
+
+}  // namespace rd

@@ -34,13 +34,21 @@ bool paper_entry(int f, KernelRef* r) {
 
 template <class OpT>
 bool lookup_sweep(int variant, int unroll, int vec_bytes, KernelRef* r) {
+  if (variant == RD_VARIANT_BULK) {
+    const int st = unroll ? unroll : 6;
+    const int sb = vec_bytes ? vec_bytes : 32768;
+    return bulk_entry<OpT, 4, 32768>(st, sb, r) || bulk_entry<OpT, 6, 32768>(st, sb, r) ||
+           bulk_entry<OpT, 3, 65536>(st, sb, r) || bulk_entry<OpT, 12, 16384>(st, sb, r) ||
+           bulk_entry<OpT, 8, 16384>(st, sb, r) || bulk_entry<OpT, 6, 16384>(st, sb, r) ||
+           bulk_entry<OpT, 24, 8192>(st, sb, r);
+  }
   if (variant == RD_VARIANT_PAPER) {
     const int f = unroll ? unroll : 8;
     return paper_entry<OpT, 1>(f, r) || paper_entry<OpT, 2>(f, r) || paper_entry<OpT, 3>(f, r) ||
            paper_entry<OpT, 4>(f, r) || paper_entry<OpT, 5>(f, r) || paper_entry<OpT, 6>(f, r) ||
            paper_entry<OpT, 7>(f, r) || paper_entry<OpT, 8>(f, r) || paper_entry<OpT, 16>(f, r);
   }
-  if (variant != RD_VARIANT_VECTOR && variant != RD_VARIANT_AUTO) return false;
+  if (variant != RD_VARIANT_VECTOR) return false;   // AUTO resolves to the default kernels
   const int u = unroll ? unroll : kDefaultUnroll4;
   const int vb = vec_bytes ? vec_bytes : kDefaultVec;
   return vec_row<OpT, 4>(u, vb, r) || vec_row<OpT, 8>(u, vb, r) || vec_row<OpT, 16>(u, vb, r) ||

@@ -40,6 +40,10 @@ struct KArgs {
   unsigned* ticket;         // zero between launches (workspace)
   uint32_t tag;             // record tag
   int mode;                 // 0 = value, 1 = record
+  // bulk variant only
+  uint64_t chunk_bytes;     // bytes per chunk (a multiple of the stage size)
+  uint32_t nchunks;         // chunks in the body
+  unsigned* work;           // dynamic chunk counter, zero between launches
 };
 
 // ---------------------------------------------------------------- loads

@@ -1,5 +1,6 @@
 // rd_registry.h -- compiled kernel configurations, looked up by the planner.
 #pragma once
+#include "rd_bulk.cuh"
 #include "rd_kernels.cuh"
 
 namespace rd {
@@ -10,6 +11,7 @@ using CombineFn = void (*)(const rd_record*, int, uint32_t, void*, rd_record*, i
 struct KernelRef {
   ReduceFn fn;
   int block, unroll, vec_bytes, variant;
+  int smem_bytes = 0;   // dynamic shared memory (bulk variant: the ring)
 };
 
 constexpr int kBlock = 256;          // threads per CTA for every reduce kernel
@@ -25,11 +27,34 @@ bool lookup_float(int dtype, int op, int variant, int unroll, int vec_bytes, Ker
 bool lookup_ablation(int dtype, int op, int variant, int unroll, int vec_bytes, KernelRef* r);
 CombineFn lookup_combine(int dtype, int op);
 
-// Helpers used by the instantiation units.
+// bulk variant: CW consumer warps + 1 producer warp per CTA
+constexpr int kBulkConsumerWarps = 8;
+
+template <class OpT, int STAGES, int STAGE_BYTES>
+inline bool bulk_entry(int stages, int stage_bytes, KernelRef* r) {
+  if (stages != STAGES || stage_bytes != STAGE_BYTES) return false;
+  *r = KernelRef{rd_bulk_kernel<OpT, STAGES, STAGE_BYTES, kBulkConsumerWarps>, 32 * (kBulkConsumerWarps + 1),
+                 STAGES, STAGE_BYTES, RD_VARIANT_BULK,
+                 BulkSmem<STAGES, STAGE_BYTES, kBulkConsumerWarps>::kBytes};
+  return true;
+}
+
+// Default bulk ring (chosen by the stage sweep): 4 x 32 KB.
+constexpr int kBulkStages = 4;
+constexpr int kBulkStageBytes = 32768;
+// AUTO picks the bulk pipeline at or above this many input bytes (below it the
+// vector kernel's shorter latency chain wins).
+constexpr uint64_t kBulkMinBytes = 32ull << 20;
+
+// Helpers used by the instantiation units: the default kernels of one (dtype, op).
 template <class OpT>
 inline bool lookup_default(int variant, int unroll, int vec_bytes, KernelRef* r) {
   using T = typename OpT::T;
   constexpr int du = sizeof(T) == 4 ? kDefaultUnroll4 : kDefaultUnroll8;
+  if (variant == RD_VARIANT_BULK) {
+    return bulk_entry<OpT, kBulkStages, kBulkStageBytes>(unroll ? unroll : kBulkStages,
+                                                         vec_bytes ? vec_bytes : kBulkStageBytes, r);
+  }
   if (variant != RD_VARIANT_AUTO && variant != RD_VARIANT_VECTOR) return false;
   const int u = unroll ? unroll : du;
   const int vb = vec_bytes ? vec_bytes : kDefaultVec;

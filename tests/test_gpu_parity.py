@@ -80,6 +80,26 @@ def test_misaligned_bases(rd, dtype, op):
             _parity.check(val(rd.reduce(to_dev(x, off), op)), x, op)
 
 
+@pytest.mark.parametrize("dtype,op", PAIRS, ids=[f"{d}-{o}" for d, o in PAIRS])
+def test_bulk_variant_all_pairs(rd, dtype, op):
+    """The bulk-copy pipeline (AUTO's choice for large inputs) on every pair, at
+    sizes with partial stages/chunks and misaligned bases, forced on small n too."""
+    wl = inputs.default_workload(dtype, op)
+    for n in (0, 1, 7, 4099, 65536 + 3, (1 << 21) + 1, (1 << 23) + 5):
+        x = inputs.generate(n, dtype, wl, seed=n % 3 + 1)
+        for off in (0, 1):
+            out, info = rd.reduce_ex(to_dev(x, off), op, variant="bulk")
+            assert info["variant"] == "bulk"
+            _parity.check(val(out), x, op)
+
+
+def test_auto_planner_choice(rd):
+    small = to_dev(inputs.generate(1 << 20, "float32", "u01"))
+    big = torch.empty(1 << 24, dtype=torch.float32, device="cuda")
+    assert rd.reduce_ex(small, "sum")[1]["variant"] == "vector"
+    assert rd.reduce_ex(big.zero_(), "sum")[1]["variant"] == "bulk"
+
+
 @pytest.mark.parametrize("dtype,op", [("float32", "sum"), ("int64", "prod"), ("float64", "max"),
                                       ("uint32", "min"), ("float64", "prod"), ("int32", "xor")])
 def test_forced_grids(rd, dtype, op):
@@ -87,10 +107,11 @@ def test_forced_grids(rd, dtype, op):
     wl = inputs.default_workload(dtype, op)
     x = inputs.generate((1 << 20) + 5, dtype, wl, seed=5)
     xd = to_dev(x, 3)
-    for g in (1, 2, 3, 7, 148, 593, 1000, 4096):
-        out, info = rd.reduce_ex(xd, op, grid=g)
-        assert info["grid"] == g
-        _parity.check(val(out), x, op)
+    for variant in ("vector", "bulk"):
+        for g in (1, 2, 3, 7, 148, 593, 1000, 4096):
+            out, info = rd.reduce_ex(xd, op, variant=variant, grid=g)
+            assert info["grid"] == g
+            _parity.check(val(out), x, op)
 
 
 @pytest.mark.parametrize("dtype", ["float32", "int32"])
@@ -109,6 +130,31 @@ def test_ablation_configs(rd, dtype):
             out, info = rd.reduce_ex(xd, "sum", variant="paper", unroll=f)
             assert info["variant"] == "paper" and info["unroll"] == f
             _parity.check(val(out), x, "sum")
+        for st, sb in BULK_CONFIGS:
+            out, info = rd.reduce_ex(xd, "sum", variant="bulk", unroll=st, vec_bytes=sb)
+            assert info["variant"] == "bulk"
+            _parity.check(val(out), x, "sum")
+
+
+BULK_CONFIGS = [(4, 32768), (6, 32768), (3, 65536), (12, 16384), (8, 16384), (6, 16384), (24, 8192)]
+
+
+@pytest.mark.parametrize("dtype", ["float32", "int32"])
+def test_bulk_variant_sizes_and_alignment(rd, dtype):
+    """Bulk-copy pipeline: partial stages, partial chunks, empty body, head/tail,
+    and deterministic results (the per-chunk tree does not depend on scheduling)."""
+    wl = "normalish" if dtype == "float32" else "uniform_bits"
+    for n in (0, 1, 3, 4, 5, 17, 1000, 8191, 8193, 65536 + 5, (1 << 20) + 3, 5533214, (1 << 26) + 7):
+        x = inputs.generate(n, dtype, wl, seed=n % 5 + 1)
+        for off in (0, 1, 3):
+            xd = to_dev(x, off)
+            for st, sb in BULK_CONFIGS[:2] + BULK_CONFIGS[-1:]:
+                outs = set()
+                for rep in range(3):
+                    out, info = rd.reduce_ex(xd, "sum", variant="bulk", unroll=st, vec_bytes=sb)
+                    outs.add(val(out).tobytes())
+                    _parity.check(val(out), x, "sum")
+                assert len(outs) == 1, "bulk variant must be deterministic"
 
 
 # ------------------------------------------------------------------ special values

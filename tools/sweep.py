@@ -1,0 +1,207 @@
+#!/usr/bin/env python
+"""Measurement sweeps on one B200 (run under gpurun); writes JSON to --out.
+
+    python tools/sweep.py probe      --out gpurun_out/probe.json     # HBM read-bandwidth probe
+    python tools/sweep.py ablation   --out gpurun_out/ablation.json  # U x VB and paper F (Table 2 on B200)
+    python tools/sweep.py ops        --out gpurun_out/ops.json       # all 29 (dtype, op) pairs
+    python tools/sweep.py sizes      --out gpurun_out/sizes.json     # n = 2^10 .. 2^30
+
+Timing: CUDA events on the launching stream around each launch, after
+warm-up; when the input is smaller than 4x L2 the L2 is flushed (a 512 MiB
+memset) before every timed launch. GB/s = n * sizeof(dtype) / t (decimal,
+PAPER.md Table 2's convention).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+import paper_1710_07358_b200 as rd  # noqa: E402
+
+L2_BYTES = 126 * 2 ** 20
+SIZE = {"int32": 4, "uint32": 4, "int64": 8, "float32": 4, "float64": 8}
+_flush = None
+
+
+def flush_l2():
+    """Evict the input from L2 by READING a 512 MiB buffer (a write-based flush
+    would leave ~126 MB of dirty lines whose write-back the timed kernel pays)."""
+    global _flush
+    if _flush is None:
+        _flush = torch.ones(128 * 2 ** 20, dtype=torch.int32, device="cuda")
+    _flush.max()
+
+
+def time_launch(fn, nbytes, reps=30, warm=5):
+    s = torch.cuda.current_stream()
+    need_flush = nbytes < 4 * L2_BYTES
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        if need_flush:
+            flush_l2()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        fn()
+        b.record(s)
+        b.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    med = statistics.median(ts)
+    return {"t_med_us": med * 1e6, "t_min_us": min(ts) * 1e6, "t_mean5_us": statistics.mean(ts[:5]) * 1e6,
+            "gbps_med": nbytes / med / 1e9, "gbps_best": nbytes / min(ts) / 1e9, "l2_flushed": need_flush}
+
+
+def make(n, dtype, wl, seed=1):
+    x = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
+    inputs.fill_device(x, wl, seed=seed)
+    return x
+
+
+def do_probe(args):
+    lib = ctypes.CDLL(os.path.join(ROOT, "tools", "libprobe.so"))
+    lib.probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    nbytes = 1 << 30
+    x = make(nbytes // 4, "float32", "u01")
+    sink = torch.zeros(1024, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    rows = []
+    for threads in (256, 512, 1024):
+        for u in (1, 2, 4, 8):
+            occ = lib.probe_occupancy(u, threads)
+            for waves in (1, 2, 4):
+                for mode in (0, 1):
+                    blocks = 148 * occ * waves
+                    fn = lambda: lib.probe_read(x.data_ptr(), nbytes, u, blocks, threads, sink.data_ptr(), st, mode)
+                    r = time_launch(fn, nbytes)
+                    r.update({"threads": threads, "unroll": u, "ctas_per_sm": occ, "waves": waves,
+                              "mode": ["grid-stride", "cta-contiguous"][mode], "grid": blocks})
+                    rows.append(r)
+                    print(json.dumps(r), flush=True)
+    best = max(rows, key=lambda r: r["gbps_med"])
+    # torch copy (the MEASURED_PEAKS method) for comparison, read+write bytes
+    y = torch.empty_like(x)
+    cp = time_launch(lambda: y.copy_(x), 2 * nbytes)
+    return {"rows": rows, "best": best, "torch_copy_rw": cp}
+
+
+def do_ablation(args):
+    out = {}
+    for dtype in ("float32", "int32"):
+        wl = "u01" if dtype == "float32" else "uniform_bits"
+        for n in (1 << 28, 5533214):
+            x = make(n, dtype, wl)
+            o = torch.empty((), dtype=x.dtype, device="cuda")
+            rows = []
+            cfgs = [("vector", u, vb) for vb in (4, 8, 16, 32) for u in (1, 2, 3, 4, 5, 6, 7, 8, 16)]
+            cfgs += [("paper", u, 0) for u in (1, 2, 3, 4, 5, 6, 7, 8, 16)]
+            cfgs += [("bulk", st, sb) for st, sb in ((4, 32768), (6, 32768), (3, 65536), (12, 16384),
+                                                     (8, 16384), (6, 16384), (24, 8192))]
+            if args.only:
+                cfgs = [c for c in cfgs if c[0] in args.only]
+            for variant, u, vb in cfgs:
+                if True:
+                        _, info = rd.reduce_ex(x, "sum", variant=variant, unroll=u, vec_bytes=vb, out=o)
+                        fn = lambda: rd.reduce_ex(x, "sum", variant=variant, unroll=u, vec_bytes=vb, out=o)
+                        r = time_launch(fn, n * 4)
+                        r.update({"variant": variant, "unroll": u, "vec_bytes": info["vec_bytes"],
+                                  "grid": info["grid"], "regs": info["regs_per_thread"],
+                                  "ctas_per_sm": info["ctas_per_sm"]})
+                        rows.append(r)
+                        print(dtype, n, json.dumps(r), flush=True)
+            out[f"{dtype}-{n}"] = rows
+            del x
+    return out
+
+
+def do_ops(args):
+    rows = []
+    pairs = [(d, o) for d in ("int32", "uint32", "int64") for o in rd.OPS] + \
+            [(d, o) for d in ("float32", "float64") for o in ("sum", "prod", "min", "max")]
+    for log2n in args.log2n:
+        n = 1 << log2n
+        for dtype, op in pairs:
+            x = make(n, dtype, inputs.default_workload(dtype, op))
+            o = torch.empty((), dtype=x.dtype, device="cuda")
+            _, info = rd.reduce_ex(x, op, out=o)
+            r = time_launch(lambda: rd.reduce(x, op, out=o), n * SIZE[dtype])
+            r.update({"dtype": dtype, "op": op, "n": n, "grid": info["grid"], "regs": info["regs_per_thread"],
+                      "ctas_per_sm": info["ctas_per_sm"]})
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            del x
+    return rows
+
+
+def do_sizes(args):
+    rows = []
+    for dtype in ("float32", "int32"):
+        for log2n in range(10, 31):
+            n = 1 << log2n
+            x = make(n, dtype, "u01" if dtype == "float32" else "uniform_bits")
+            o = torch.empty((), dtype=x.dtype, device="cuda")
+            r = time_launch(lambda: rd.reduce(x, "sum", out=o), n * 4, reps=50)
+            # launch-bound regime: also time 100 back-to-back launches (no flush)
+            s = torch.cuda.current_stream()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            for _ in range(100):
+                rd.reduce(x, "sum", out=o)
+            b.record(s)
+            b.synchronize()
+            r.update({"dtype": dtype, "n": n, "batched100_us_per_launch": a.elapsed_time(b) * 10.0})
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            del x
+    return rows
+
+
+def do_grids(args):
+    """Grid multiplier (waves of resident CTAs) for the default kernels at n = 2^28."""
+    rows = []
+    for dtype, op in (("float32", "sum"), ("int32", "sum"), ("float64", "sum"), ("float32", "max")):
+        n = 1 << 28
+        x = make(n, dtype, inputs.default_workload(dtype, op))
+        o = torch.empty((), dtype=x.dtype, device="cuda")
+        _, info = rd.reduce_ex(x, op, out=o)
+        g0 = info["grid"]
+        for mult in (0.5, 1, 2, 3, 4, 8):
+            g = max(1, int(g0 * mult))
+            _, info = rd.reduce_ex(x, op, grid=g, out=o)
+            r = time_launch(lambda: rd.reduce_ex(x, op, grid=g, out=o), n * SIZE[dtype])
+            r.update({"dtype": dtype, "op": op, "grid": g, "mult": mult})
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+        del x
+    return rows
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids"])
+    p.add_argument("--out", required=True)
+    p.add_argument("--log2n", type=int, nargs="+", default=[28])
+    p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
+    args = p.parse_args()
+    res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
+           "grids": do_grids}[args.what](args)
+    meta = {"device": torch.cuda.get_device_name(), "what": args.what}
+    with open(args.out, "w") as f:
+        json.dump({"meta": meta, "result": res}, f, indent=1)
+
+if __name__ == "__main__":
+    main()
+
+
