@@ -167,6 +167,21 @@ def release_workspaces():
     check(lib().rd_release_workspaces(), "rd_release_workspaces")
 
 
+def broadcast_unique_id(group=None):
+    """rank 0 of the process group draws an NCCL unique id (rd_get_unique_id);
+    every rank returns the same 128 bytes as an rd_unique_id."""
+    import torch.distributed as dist
+    uid = _lib.rd_unique_id()
+    if dist.get_rank(group) == 0:
+        check(lib().rd_get_unique_id(ctypes.byref(uid)), "rd_get_unique_id")
+    # the raw 128 bytes (uid.internal would stop at the first NUL)
+    obj = [ctypes.string_at(ctypes.addressof(uid), 128) if dist.get_rank(group) == 0 else None]
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast_object_list(obj, src=src, group=group)
+    ctypes.memmove(ctypes.addressof(uid), obj[0], 128)
+    return uid
+
+
 class Comm:
     """One NCCL communicator per process/GPU for reduce_multi."""
 
@@ -181,13 +196,7 @@ class Comm:
         import torch.distributed as dist
         rank, nranks = dist.get_rank(group), dist.get_world_size(group)
         dev = torch.cuda.current_device() if device is None else device
-        uid = _lib.rd_unique_id()
-        if rank == 0:
-            check(lib().rd_get_unique_id(ctypes.byref(uid)), "rd_get_unique_id")
-        # the raw 128 bytes (uid.internal would stop at the first NUL)
-        obj = [ctypes.string_at(ctypes.addressof(uid), 128) if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        ctypes.memmove(ctypes.addressof(uid), obj[0], 128)
+        uid = broadcast_unique_id(group)
         h = ctypes.c_void_p()
         check(lib().rd_comm_init(ctypes.byref(h), nranks, rank, ctypes.byref(uid), dev), "rd_comm_init")
         return cls(h.value, nranks, rank, dev)
