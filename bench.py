@@ -214,21 +214,20 @@ def run_b200(args):
         torch.cuda.synchronize(dev)
 
     # ---------------- timed region: exactly K steps
+    # (no per-step events: an event between two launches would serialise them
+    # and hide the programmatic-dependent-launch overlap of consecutive steps)
     K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     barrier()
     t0.record(stream)
     for i in range(K):
-        ev[i][0].record(stream)
         step()
-        ev[i][1].record(stream)
     t1.record(stream)
     barrier()
     clocks = sampler.stop()
     total_ms = t0.elapsed_time(t1)
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+    local_ms = total_ms
     if ws > 1:
         import torch.distributed as dist
         tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
@@ -238,18 +237,18 @@ def run_b200(args):
 
     # ---------------- dominant kernel (the reduce kernel) alone, for the roofline
     if comm is None:
-        kern_ms = statistics.mean(step_ms)          # one launch per step
-        kern_src = "per-step CUDA events in the timed region (1 launch per step)"
+        kern_ms = local_ms / K                      # one launch per step
+        kern_src = "CUDA events around the K back-to-back steps of the timed region / K (1 launch per step)"
     else:
         rec = torch.empty(32, dtype=torch.uint8, device=dev)
-        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
         for i in range(K):
-            kev[i][0].record(stream)
             rd.reduce_partial(x, op, rec=rec)
-            kev[i][1].record(stream)
+        b.record(stream)
         torch.cuda.synchronize(dev)
-        kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
-        kern_src = "CUDA events around the same reduce kernel (reduce_partial), K launches after the timed region"
+        kern_ms = a.elapsed_time(b) / K
+        kern_src = "CUDA events around K back-to-back launches of the same reduce kernel (reduce_partial) / K"
     peak, peak_src = load_peaks()
     achieved = gbps(n * s, kern_ms / 1e3)
 

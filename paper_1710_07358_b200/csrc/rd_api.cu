@@ -69,13 +69,13 @@ rd_status get_workspace(int dev, cudaStream_t stream, Workspace* out) {
   }
   Workspace w;
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, sizeof(Slot) * kMaxGrid + 256);
+  cudaError_t e = cudaMalloc(&p, sizeof(Slot) * kMaxSlots + 256);
   if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
-  e = cudaMemset(p, 0, sizeof(Slot) * kMaxGrid + 256);
+  e = cudaMemset(p, 0, sizeof(Slot) * kMaxSlots + 256);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "workspace init"); }
   w.partials = (Slot*)p;
-  w.ticket = (unsigned*)((char*)p + sizeof(Slot) * kMaxGrid);
+  w.ticket = (unsigned*)((char*)p + sizeof(Slot) * kMaxSlots);
   w.work = w.ticket + 32;     // separate 128-byte line
   g_ws[key] = w;
   *out = w;
@@ -195,13 +195,25 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     a.tail = 0;
   }
   if (k.variant == RD_VARIANT_BULK) {
-    // chunks of whole stages, at most kMaxGrid of them; fixed by n and alignment only
-    const uint64_t body_bytes = a.nvec * 16;
-    const uint64_t stage = (uint64_t)k.vec_bytes;
-    uint64_t stages_per_chunk = (body_bytes + stage * kMaxGrid - 1) / (stage * kMaxGrid);
-    if (stages_per_chunk < 4) stages_per_chunk = 4;
-    a.chunk_bytes = stages_per_chunk * stage;
-    a.nchunks = (uint32_t)((body_bytes + a.chunk_bytes - 1) / a.chunk_bytes);
+    // Chunk schedule, fixed by n and the base alignment only (determinism):
+    // a head region in chunks of C0 (about 12 per SM, at most ~6000), then a
+    // tail region of ~148*4 chunks of C1 = 2 stages, so the dynamic schedule
+    // ends with short chunks and the per-SM tail imbalance is < one C1 chunk.
+    const uint64_t T = a.nvec * 16;
+    const uint64_t S = (uint64_t)k.vec_bytes;
+    const uint64_t C1 = 2 * S;
+    const uint64_t R = T < 148ull * 4 * C1 ? T : 148ull * 4 * C1;
+    uint64_t c0 = T / (148ull * 12);
+    if (c0 < T / 6000) c0 = T / 6000;
+    c0 = (c0 + S - 1) / S * S;
+    if (c0 < 4 * S) c0 = 4 * S;
+    const uint64_t nhead = (T - R) / c0;
+    const uint64_t ntail = (T - nhead * c0 + C1 - 1) / C1;
+    a.chunk_bytes = c0;
+    a.tail_chunk_bytes = C1;
+    a.nhead_chunks = (uint32_t)nhead;
+    a.nchunks = (uint32_t)(nhead + ntail);
+    if (a.nchunks > (uint32_t)kMaxSlots) { set_error("chunk schedule exceeds the workspace"); return RD_ERR_INVALID_ARG; }
     a.work = ws.work;
     uint64_t need = a.nchunks ? a.nchunks : 1;
     if (g > need) g = need;
@@ -225,8 +237,21 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   a.tag = record_tag(dtype, op);
   a.mode = mode;
 
-  k.fn<<<(unsigned)g, k.block, k.smem_bytes, stream>>>(a);
-  e = cudaGetLastError();
+  // programmatic dependent launch: the grid may be scheduled while the previous
+  // kernel on the stream drains; the kernels call griddepcontrol.wait before
+  // touching global memory (rd_kernels.cuh pdl_wait).
+  cudaLaunchConfig_t lc;
+  std::memset(&lc, 0, sizeof(lc));
+  lc.gridDim = dim3((unsigned)g);
+  lc.blockDim = dim3((unsigned)k.block);
+  lc.dynamicSmemBytes = (size_t)k.smem_bytes;
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  e = cudaLaunchKernelEx(&lc, k.fn, a);
   if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
   if (info) {
     std::memset(info, 0, sizeof(*info));

@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
 
   const unsigned char* body = args.x + args.head * sizeof(T);
   const uint64_t body_bytes = args.nvec * 16;
+  pdl_wait();
 
   if (warp == CW) {
     // ---------------------------------------------------------------- producer
@@ -123,8 +124,9 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
           mbar_arrive(&full[stage]);
           break;
         }
-        const uint64_t cbeg = (uint64_t)c * args.chunk_bytes;
-        const uint64_t cend = min(cbeg + args.chunk_bytes, body_bytes);
+        uint64_t cbeg, clen;
+        chunk_range(args, c, body_bytes, &cbeg, &clen);
+        const uint64_t cend = cbeg + clen;
         for (uint64_t off = cbeg; off < cend; off += STAGE_BYTES) {
           const uint32_t bytes = (uint32_t)min((uint64_t)STAGE_BYTES, cend - off);
           mbar_wait(&empty[stage], phase ^ 1);
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
     }
   }
   // ------------------------------------------------------------------ grid combine
+  pdl_trigger();
   __syncthreads();
   __shared__ unsigned s_last;
   if (threadIdx.x == 0) {
@@ -212,11 +215,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  Acc b = OpT::identity();
-  for (uint32_t j = threadIdx.x; j < args.nchunks; j += B) {
-    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(args.partials + j));
-    b = OpT::combine(b, OpT::unpack(Slot{v.x, v.y}));
-  }
+  Acc b = fold_slots<OpT, B>(args.partials, args.nchunks);
   if (threadIdx.x < args.head) b = OpT::fold(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)));
   if (threadIdx.x < args.tail)
     b = OpT::fold(b, ldg_scalar<T>(args.x + (args.tail_start + threadIdx.x) * sizeof(T)));

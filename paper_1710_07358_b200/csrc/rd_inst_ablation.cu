@@ -35,8 +35,8 @@ bool paper_entry(int f, KernelRef* r) {
 template <class OpT>
 bool lookup_sweep(int variant, int unroll, int vec_bytes, KernelRef* r) {
   if (variant == RD_VARIANT_BULK) {
-    const int st = unroll ? unroll : 6;
-    const int sb = vec_bytes ? vec_bytes : 32768;
+    const int st = unroll ? unroll : kBulkStages;
+    const int sb = vec_bytes ? vec_bytes : kBulkStageBytes;
     return bulk_entry<OpT, 4, 32768>(st, sb, r) || bulk_entry<OpT, 6, 32768>(st, sb, r) ||
            bulk_entry<OpT, 3, 65536>(st, sb, r) || bulk_entry<OpT, 12, 16384>(st, sb, r) ||
            bulk_entry<OpT, 8, 16384>(st, sb, r) || bulk_entry<OpT, 6, 16384>(st, sb, r) ||

@@ -40,11 +40,34 @@ struct KArgs {
   unsigned* ticket;         // zero between launches (workspace)
   uint32_t tag;             // record tag
   int mode;                 // 0 = value, 1 = record
-  // bulk variant only
-  uint64_t chunk_bytes;     // bytes per chunk (a multiple of the stage size)
+  // bulk variant only: the chunk schedule (fixed by n and the base alignment)
+  uint64_t chunk_bytes;     // head-region chunk size C0 (a multiple of the stage size)
+  uint64_t tail_chunk_bytes;// tail-region chunk size C1 (smaller: short tail imbalance)
   uint32_t nchunks;         // chunks in the body
+  uint32_t nhead_chunks;    // chunks of size C0; the rest have size C1
   unsigned* work;           // dynamic chunk counter, zero between launches
 };
+
+// Programmatic dependent launch: a kernel launched right behind another may be
+// scheduled while the previous grid drains; it must not touch global memory
+// before griddepcontrol.wait (which returns once the previous grid completed
+// and its writes are visible). launch_dependents lets the NEXT grid be
+// scheduled early. Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// chunk c of the bulk schedule -> [off, off + len) of the body
+__device__ __forceinline__ void chunk_range(const struct KArgs& a, uint32_t c, uint64_t body_bytes,
+                                            uint64_t* off, uint64_t* len) {
+  if (c < a.nhead_chunks) {
+    *off = (uint64_t)c * a.chunk_bytes;
+    *len = a.chunk_bytes;
+  } else {
+    const uint64_t head_bytes = (uint64_t)a.nhead_chunks * a.chunk_bytes;
+    *off = head_bytes + (uint64_t)(c - a.nhead_chunks) * a.tail_chunk_bytes;
+    *len = min(a.tail_chunk_bytes, body_bytes - *off);
+  }
+}
 
 // ---------------------------------------------------------------- loads
 template <int VB> struct Vec { uint32_t w[VB / 4]; };
@@ -125,6 +148,26 @@ __device__ __forceinline__ void finish(const typename OpT::Acc& a, const KArgs& 
   }
 }
 
+// Thread t folds slots t, t+B, t+2B, ... in increasing order (a fixed tree);
+// 8 independent loads in flight per thread.
+template <class OpT, int B>
+__device__ __forceinline__ typename OpT::Acc fold_slots(const Slot* slots, uint32_t count) {
+  using Acc = typename OpT::Acc;
+  Acc b = OpT::identity();
+  for (uint32_t j0 = threadIdx.x; j0 < count; j0 += 8 * B) {
+    ulonglong2 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t j = j0 + k * B;
+      v[k] = (j < count) ? __ldcg(reinterpret_cast<const ulonglong2*>(slots + j)) : make_ulonglong2(0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (j0 + k * B < count) b = OpT::combine(b, OpT::unpack(Slot{v[k].x, v[k].y}));
+  }
+  return b;
+}
+
 // a6: one partial per CTA, the last CTA to arrive folds them in index order.
 template <class OpT, int B>
 __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& args,
@@ -145,11 +188,7 @@ __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& a
   __syncthreads();
   if (!s_last) return;
   __threadfence();                                     // acquire the other partials
-  Acc b = OpT::identity();
-  for (unsigned j = threadIdx.x; j < gridDim.x; j += B) {
-    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(args.partials + j));
-    b = OpT::combine(b, OpT::unpack(Slot{v.x, v.y}));
-  }
+  Acc b = fold_slots<OpT, B>(args.partials, gridDim.x);
   b = block_reduce<OpT, B>(b, smem);
   if (threadIdx.x == 0) {
     finish<OpT>(b, args);
@@ -173,6 +212,7 @@ __global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
   const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * B;
   const unsigned char* body = args.x + args.head * sizeof(T);
+  pdl_wait();
   const uint64_t nvec = args.nvec;
   uint64_t i = tid;
   if constexpr (U > 1) {
@@ -194,6 +234,7 @@ __global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
   // a2: head and tail stragglers
   if (tid < args.head) acc[0] = OpT::fold(acc[0], ldg_scalar<T>(args.x + tid * sizeof(T)));
   if (tid < args.tail) acc[L - 1] = OpT::fold(acc[L - 1], ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T)));
+  pdl_trigger();
   // a3
   Acc a = acc[0];
 #pragma unroll
@@ -220,6 +261,7 @@ __global__ void __launch_bounds__(B) rd_paper_kernel(const KArgs args) {
   const uint64_t gs = (uint64_t)gridDim.x * B;
   const T* x = reinterpret_cast<const T*>(args.x);
   const uint64_t n = args.n;
+  pdl_wait();
   for (uint64_t pos = gid * F; pos < n; pos += gs * F) {
     T v[F];
 #pragma unroll

@@ -15,7 +15,8 @@ struct KernelRef {
 };
 
 constexpr int kBlock = 256;          // threads per CTA for every reduce kernel
-constexpr int kMaxGrid = 4096;       // workspace slots
+constexpr int kMaxGrid = 4096;       // CTAs at most (vector / paper variants)
+constexpr int kMaxSlots = 8192;      // workspace partial slots (per CTA, or per chunk for bulk)
 // Default configuration per element size (chosen by the U x V sweep).
 constexpr int kDefaultUnroll4 = 4;   // 4-byte elements
 constexpr int kDefaultUnroll8 = 4;   // 8-byte elements
@@ -44,7 +45,7 @@ constexpr int kBulkStages = 4;
 constexpr int kBulkStageBytes = 32768;
 // AUTO picks the bulk pipeline at or above this many input bytes (below it the
 // vector kernel's shorter latency chain wins).
-constexpr uint64_t kBulkMinBytes = 32ull << 20;
+constexpr uint64_t kBulkMinBytes = 128ull << 20;
 
 // Helpers used by the instantiation units: the default kernels of one (dtype, op).
 template <class OpT>

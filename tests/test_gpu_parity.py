@@ -95,7 +95,7 @@ def test_bulk_variant_all_pairs(rd, dtype, op):
 
 def test_auto_planner_choice(rd):
     small = to_dev(inputs.generate(1 << 20, "float32", "u01"))
-    big = torch.empty(1 << 24, dtype=torch.float32, device="cuda")
+    big = torch.empty(1 << 25, dtype=torch.float32, device="cuda")
     assert rd.reduce_ex(small, "sum")[1]["variant"] == "vector"
     assert rd.reduce_ex(big.zero_(), "sum")[1]["variant"] == "bulk"
 

@@ -161,7 +161,24 @@ def do_sizes(args):
                 rd.reduce(x, "sum", out=o)
             b.record(s)
             b.synchronize()
-            r.update({"dtype": dtype, "n": n, "batched100_us_per_launch": a.elapsed_time(b) * 10.0})
+            # ... and as a CUDA graph of 100 launches (no host launch overhead)
+            gs = torch.cuda.Stream()
+            with torch.cuda.stream(gs):
+                rd.reduce(x, "sum", out=o)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(100):
+                    rd.reduce(x, "sum", out=o)
+            g.replay()
+            torch.cuda.synchronize()
+            c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c.record(s)
+            g.replay()
+            d.record(s)
+            d.synchronize()
+            r.update({"dtype": dtype, "n": n, "batched100_us_per_launch": a.elapsed_time(b) * 10.0,
+                      "graph100_us_per_launch": c.elapsed_time(d) * 10.0})
             rows.append(r)
             print(json.dumps(r), flush=True)
             del x
@@ -188,20 +205,53 @@ def do_grids(args):
     return rows
 
 
+def do_crossover(args):
+    """vector vs bulk variant around the AUTO threshold: L2-cold single launches
+    (read-flush before each) and back-to-back launches in a CUDA graph."""
+    rows = []
+    for dtype in ("float32", "float64"):
+        for log2n in range(18, 29):
+            n = 1 << log2n
+            x = make(n, dtype, "u01")
+            o = torch.empty((), dtype=x.dtype, device="cuda")
+            for variant in ("vector", "bulk"):
+                fn = lambda: rd.reduce_ex(x, "sum", variant=variant, out=o)
+                r = time_launch(fn, n * SIZE[dtype], reps=30)
+                gs = torch.cuda.Stream()
+                with torch.cuda.stream(gs):
+                    fn()
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=gs):
+                    for _ in range(20):
+                        fn()
+                g.replay()
+                torch.cuda.synchronize()
+                s = torch.cuda.current_stream()
+                c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                c.record(s)
+                g.replay()
+                d.record(s)
+                d.synchronize()
+                r.update({"dtype": dtype, "n": n, "variant": variant, "graph_us_per_launch": c.elapsed_time(d) * 50.0})
+                rows.append(r)
+                print(json.dumps(r), flush=True)
+            del x
+    return rows
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids"])
+    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
     args = p.parse_args()
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
-           "grids": do_grids}[args.what](args)
+           "grids": do_grids, "crossover": do_crossover}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
         json.dump({"meta": meta, "result": res}, f, indent=1)
 
 if __name__ == "__main__":
     main()
-
-
