@@ -139,6 +139,13 @@ struct Float32Prod {
 };
 
 // ---------------------------------------- float64 x (double-double accumulator)
+// (hi, lo) represents hi + lo. hi is always the plainly rounded running product
+// and lo carries the exact rounding errors (TwoProduct by FMA), scaled along:
+//   fold:    hi' = fl(hi*x),  lo' = lo*x + (hi*x - hi')        (3 DP ops)
+// lo is not renormalised into hi: |lo| grows at most ~n ulp(hi), and its own
+// rounding (2^-53 |lo|) stays ~n 2^-106 |hi| -- far below the fp64 result's
+// half ulp for any n < 2^40. Zero / inf / NaN products: hi is exact in class
+// and sign, and the result is hi alone.
 struct DD { double hi, lo; };
 
 struct Float64Prod {
@@ -146,26 +153,17 @@ struct Float64Prod {
   using Acc = DD;
   static constexpr bool kFloat = true;
   __device__ __forceinline__ static Acc identity() { return DD{1.0, 0.0}; }
-  // renormalise p + e (|e| <= ulp(p)/2-ish): Fast2Sum; keep plain p for
-  // zero / inf / NaN products where the error term is meaningless.
-  __device__ __forceinline__ static Acc renorm(double p, double e) {
-    double s = __dadd_rn(p, e);
-    double l = __dsub_rn(e, __dsub_rn(s, p));
-    bool ok = (p != 0.0) && (fabs(p) < __longlong_as_double(0x7ff0000000000000LL));
-    return ok ? DD{s, l} : DD{p, 0.0};
-  }
   __device__ __forceinline__ static Acc fold(Acc a, T x) {
-    double p = __dmul_rn(a.hi, x);
-    double e = __fma_rn(a.hi, x, -p);       // exact error of a.hi * x (TwoProduct)
-    e = __fma_rn(a.lo, x, e);
-    return renorm(p, e);
+    const double p = __dmul_rn(a.hi, x);
+    const double e = __fma_rn(a.hi, x, -p);   // exact error of a.hi * x
+    return DD{p, __fma_rn(a.lo, x, e)};
   }
   __device__ __forceinline__ static Acc combine(Acc a, Acc b) {
-    double p = __dmul_rn(a.hi, b.hi);
+    const double p = __dmul_rn(a.hi, b.hi);
     double e = __fma_rn(a.hi, b.hi, -p);
     e = __fma_rn(a.hi, b.lo, e);
     e = __fma_rn(a.lo, b.hi, e);
-    return renorm(p, e);
+    return DD{p, e};
   }
   __device__ __forceinline__ static Acc warp_reduce(Acc a) {
 #pragma unroll
@@ -175,7 +173,11 @@ struct Float64Prod {
     }
     return a;
   }
-  __device__ __forceinline__ static void store(Acc a, void* out) { *(double*)out = a.hi; }
+  __device__ __forceinline__ static double value(Acc a) {
+    const bool ok = (a.hi != 0.0) && (fabs(a.hi) < __longlong_as_double(0x7ff0000000000000LL));
+    return ok ? __dadd_rn(a.hi, a.lo) : a.hi;
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) { *(double*)out = value(a); }
   __device__ __forceinline__ static void store_empty(void* out) { *(double*)out = 1.0; }
   __device__ __forceinline__ static Slot pack(Acc a) {
     return Slot{(uint64_t)__double_as_longlong(a.hi), (uint64_t)__double_as_longlong(a.lo)};

@@ -43,6 +43,10 @@ def flush_l2():
 
 
 def time_launch(fn, nbytes, reps=30, warm=5):
+    """Single launches after a synchronize (L2 read-flushed first when the input
+    is < 4x L2): median / min / mean-of-5 (the paper's Table 2 convention is a
+    mean of 5). For inputs >= 4x L2 also the steady state: `reps`
+    back-to-back launches between two events (what bench.py measures)."""
     s = torch.cuda.current_stream()
     need_flush = nbytes < 4 * L2_BYTES
     for _ in range(warm):
@@ -59,8 +63,18 @@ def time_launch(fn, nbytes, reps=30, warm=5):
         b.synchronize()
         ts.append(a.elapsed_time(b) * 1e-3)
     med = statistics.median(ts)
-    return {"t_med_us": med * 1e6, "t_min_us": min(ts) * 1e6, "t_mean5_us": statistics.mean(ts[:5]) * 1e6,
-            "gbps_med": nbytes / med / 1e9, "gbps_best": nbytes / min(ts) / 1e9, "l2_flushed": need_flush}
+    r = {"t_med_us": med * 1e6, "t_min_us": min(ts) * 1e6, "t_mean5_us": statistics.mean(ts[:5]) * 1e6,
+         "gbps_med": nbytes / med / 1e9, "gbps_best": nbytes / min(ts) / 1e9, "l2_flushed": need_flush}
+    if not need_flush:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(reps):
+            fn()
+        b.record(s)
+        b.synchronize()
+        t = a.elapsed_time(b) * 1e-3 / reps
+        r.update({"t_stream_us": t * 1e6, "gbps_stream": nbytes / t / 1e9})
+    return r
 
 
 def make(n, dtype, wl, seed=1):
