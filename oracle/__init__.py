@@ -26,7 +26,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 # restated codes (not imported from the CUDA package)
 DTYPES = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
-OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "and": 4, "or": 5, "xor": 6}
+OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "and": 4, "or": 5, "xor": 6, "argmin": 7, "argmax": 8}
 NP_DTYPES = {"int32": np.int32, "uint32": np.uint32, "int64": np.int64,
              "float32": np.float32, "float64": np.float64}
 
@@ -36,7 +36,8 @@ class OracleState(ctypes.Structure):
                 ("count", ctypes.c_uint64), ("ibits", ctypes.c_uint64),
                 ("hi", ctypes.c_double), ("lo", ctypes.c_double),
                 ("abs_hi", ctypes.c_double), ("abs_lo", ctypes.c_double),
-                ("all_negzero", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("all_negzero", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("best_idx", ctypes.c_uint64)]
 
 
 def build(force: bool = False) -> str:
@@ -68,6 +69,8 @@ def lib():
         L.or_identity.argtypes = [i32, i32, vp]
         L.or_merge.argtypes = [sp, sp]
         L.or_state_size.restype = u64
+        L.or_result_index.argtypes = [sp]
+        L.or_result_index.restype = ctypes.c_int64
         for f in (L.or_init, L.or_fold, L.or_result, L.or_reduce, L.or_identity, L.or_merge):
             f.restype = i32
         assert L.or_state_size() == ctypes.sizeof(OracleState)
@@ -86,6 +89,7 @@ class OracleResult:
     lo: float
     sum_abs: float       # sum |x_i| (floats only), for the tolerance 4*eps*sum|x|
     count: int
+    index: int = -1      # argmin / argmax only: smallest index of the best element
 
     @property
     def exact(self) -> float:
@@ -104,7 +108,8 @@ def _result(st: OracleState, dtype: str) -> OracleResult:
     hi, lo, sa = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     _check(lib().or_result(ctypes.byref(st), out.ctypes.data, ctypes.byref(hi),
                            ctypes.byref(lo), ctypes.byref(sa)))
-    return OracleResult(out[0], hi.value, lo.value, sa.value, int(st.count))
+    return OracleResult(out[0], hi.value, lo.value, sa.value, int(st.count),
+                        int(lib().or_result_index(ctypes.byref(st))))
 
 
 def reduce(x: np.ndarray, op: str) -> OracleResult:

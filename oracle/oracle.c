@@ -27,6 +27,11 @@
  *  R4  Float min/max are IEEE 754-2019 minimum/maximum: NaN propagates and
  *      -0.0 < +0.0.
  *  R5  Bitwise ops on float dtypes are rejected (status 2).
+ *  R6  argmin / argmax (the paper's consumers are
+ *      shortest paths and golden-section search): the value of
+ *      min / max under R4's order together with the SMALLEST index attaining
+ *      it; a NaN anywhere wins (value NaN, index of the first NaN); -0.0 ranks
+ *      below +0.0; empty input -> identity value and index -1.
  *
  * Parity pins for every function: tests/test_oracle_pins.py (DESIGN.md
  * "Oracle pins"). No function here is "parity unpinned".
@@ -37,7 +42,8 @@
 
 /* dtype / op / status numbers (restated, see header comment) */
 enum { OR_INT32 = 0, OR_UINT32 = 1, OR_INT64 = 2, OR_FLOAT32 = 3, OR_FLOAT64 = 4 };
-enum { OR_SUM = 0, OR_PROD = 1, OR_MIN = 2, OR_MAX = 3, OR_AND = 4, OR_OR = 5, OR_XOR = 6 };
+enum { OR_SUM = 0, OR_PROD = 1, OR_MIN = 2, OR_MAX = 3, OR_AND = 4, OR_OR = 5, OR_XOR = 6,
+       OR_ARGMIN = 7, OR_ARGMAX = 8 };
 enum { OR_OK = 0, OR_INVALID = 1, OR_UNSUPPORTED = 2 };
 
 /* Fold state; mirrored by oracle/__init__.py (ctypes). */
@@ -49,6 +55,7 @@ typedef struct {
   double abs_hi, abs_lo;/* sum_i |x_i| as double-double (tolerance input)   */
   int32_t all_negzero;  /* every float term so far is -0.0 (reading R2)     */
   int32_t pad;
+  uint64_t best_idx;    /* argmin / argmax: index of the current best (R6)  */
 } or_state;
 
 static int is_float(int dt) { return dt == OR_FLOAT32 || dt == OR_FLOAT64; }
@@ -100,9 +107,11 @@ static double ieee_max(double a, double b) {
   return a;
 }
 
+static int is_arg(int op) { return op == OR_ARGMIN || op == OR_ARGMAX; }
+
 int or_init(or_state* st, int dtype, int op) {
-  if (!st || dtype < 0 || dtype > 4 || op < 0 || op > 6) return OR_INVALID;
-  if (is_float(dtype) && op >= OR_AND) return OR_UNSUPPORTED; /* R5 */
+  if (!st || dtype < 0 || dtype > 4 || op < 0 || op > 8) return OR_INVALID;
+  if (is_float(dtype) && op >= OR_AND && !is_arg(op)) return OR_UNSUPPORTED; /* R5 */
   memset(st, 0, sizeof(*st));
   st->dtype = dtype;
   st->op = op;
@@ -137,9 +146,44 @@ static uint64_t int_combine(int dt, int op, uint64_t a, uint64_t b) {
   }
 }
 
+/* R6: is candidate a strictly better than the current best b? (ties keep b,
+ * the earlier index) */
+static int int_better(int dt, int op, uint64_t a, uint64_t b) {
+  int lt, gt;
+  if (dt == OR_INT64) { lt = (int64_t)a < (int64_t)b; gt = (int64_t)a > (int64_t)b; }
+  else if (dt == OR_INT32) { lt = (int32_t)(uint32_t)a < (int32_t)(uint32_t)b; gt = (int32_t)(uint32_t)a > (int32_t)(uint32_t)b; }
+  else { lt = (uint32_t)a < (uint32_t)b; gt = (uint32_t)a > (uint32_t)b; }
+  return op == OR_ARGMIN ? lt : gt;
+}
+static int float_better(int op, double a, double b) {
+  if (isnan(b)) return 0;                 /* a NaN best is never displaced */
+  if (isnan(a)) return 1;                 /* the first NaN wins */
+  if (op == OR_ARGMIN) {
+    if (a < b) return 1;
+    return a == 0.0 && b == 0.0 && signbit(a) && !signbit(b);   /* -0 < +0 */
+  }
+  if (a > b) return 1;
+  return a == 0.0 && b == 0.0 && !signbit(a) && signbit(b);
+}
+
 /* Algorithm 1, body of the `for i <- 1 to n` loop, one element. */
 static void fold_one(or_state* st, const unsigned char* p) {
   const int dt = st->dtype, op = st->op;
+  if (is_arg(op)) {
+    if (!is_float(dt)) {
+      uint64_t v = 0;
+      if (dt == OR_INT64) memcpy(&v, p, 8);
+      else { uint32_t w; memcpy(&w, p, 4); v = w; }
+      if (st->count == 0 || int_better(dt, op, v, st->ibits)) { st->ibits = v; st->best_idx = st->count; }
+    } else {
+      double x;
+      if (dt == OR_FLOAT32) { float f; memcpy(&f, p, 4); x = (double)f; }
+      else memcpy(&x, p, 8);
+      if (st->count == 0 || float_better(op, x, st->hi)) { st->hi = x; st->best_idx = st->count; }
+    }
+    st->count++;
+    return;
+  }
   if (!is_float(dt)) {
     uint64_t v = 0;
     if (dt == OR_INT64) memcpy(&v, p, 8);
@@ -182,9 +226,12 @@ int or_fold(or_state* st, const void* x, uint64_t n) {
   return OR_OK;
 }
 
-/* Result of an empty fold: Algorithm 1's initial accumulator (R1). */
+/* Result of an empty fold: Algorithm 1's initial accumulator (R1); argmin /
+ * argmax report the min / max identity value (their index is -1). */
 int or_identity(int dtype, int op, void* out) {
-  if (!out || dtype < 0 || dtype > 4 || op < 0 || op > 6) return OR_INVALID;
+  if (!out || dtype < 0 || dtype > 4 || op < 0 || op > 8) return OR_INVALID;
+  if (op == OR_ARGMIN) op = OR_MIN;
+  if (op == OR_ARGMAX) op = OR_MAX;
   if (is_float(dtype) && op >= OR_AND) return OR_UNSUPPORTED;
   if (dtype == OR_FLOAT32 || dtype == OR_FLOAT64) {
     double v = (op == OR_SUM) ? 0.0 : (op == OR_PROD) ? 1.0 : (op == OR_MIN) ? INFINITY : -INFINITY;
@@ -214,6 +261,15 @@ int or_result(const or_state* st, void* value_out, double* hi, double* lo, doubl
   if (st->count == 0) {
     or_identity(st->dtype, st->op, value_out);
     if (hi) { double v = 0.0; if (is_float(st->dtype)) { if (st->dtype == OR_FLOAT32) { float f; memcpy(&f, value_out, 4); v = f; } else memcpy(&v, value_out, 8); } *hi = v; }
+    if (lo) *lo = 0.0;
+    if (sum_abs) *sum_abs = 0.0;
+    return OR_OK;
+  }
+  if (is_arg(st->op) && is_float(st->dtype)) {
+    double v = st->hi;
+    if (st->dtype == OR_FLOAT32) { float f = (float)v; memcpy(value_out, &f, 4); }
+    else memcpy(value_out, &v, 8);
+    if (hi) *hi = v;
     if (lo) *lo = 0.0;
     if (sum_abs) *sum_abs = 0.0;
     return OR_OK;
@@ -258,6 +314,17 @@ int or_merge(or_state* a, const or_state* b) {
   if (b->count == 0) return OR_OK;
   if (a->count == 0) { *a = *b; return OR_OK; }
   const int dt = a->dtype, op = a->op;
+  if (is_arg(op)) {
+    /* b covers the block after a: its indices shift by a->count; ties keep a */
+    if (!is_float(dt)) {
+      if (int_better(dt, op, b->ibits, a->ibits)) { a->ibits = b->ibits; a->best_idx = a->count + b->best_idx; }
+    } else if (float_better(op, b->hi, a->hi)) {
+      a->hi = b->hi;
+      a->best_idx = a->count + b->best_idx;
+    }
+    a->count += b->count;
+    return OR_OK;
+  }
   if (!is_float(dt)) {
     a->ibits = int_combine(dt, op, a->ibits, b->ibits);
   } else {
@@ -287,6 +354,12 @@ int or_merge(or_state* a, const or_state* b) {
   }
   a->count += b->count;
   return OR_OK;
+}
+
+/* argmin / argmax: index of the best element (R6), -1 for an empty fold. */
+int64_t or_result_index(const or_state* st) {
+  if (!st || st->count == 0) return -1;
+  return (int64_t)st->best_idx;
 }
 
 uint64_t or_state_size(void) { return (uint64_t)sizeof(or_state); }

@@ -368,3 +368,77 @@ def test_bitwise_on_float_rejected():
     for op in ("and", "or", "xor"):
         with pytest.raises(oracle.OracleError):
             oracle.reduce(np.ones(3, np.float32), op)
+
+
+# ------------------------------------------------------ argmin / argmax (f4, reading R6)
+def _ref_arg(values, op):
+    """Independent definition: smallest index attaining the min/max under the
+    total order NaN-first, then value, then -0 < +0."""
+    def key(i):
+        v = float(values[i])
+        if math.isnan(v):
+            return (0, 0.0, 0, i)
+        neg0 = 1 if (v == 0.0 and math.copysign(1.0, v) < 0) else 0
+        if op == "argmin":
+            return (1, v, 0 if neg0 else 1, i)
+        return (1, -v, 1 if neg0 else 0, i)
+    return min(range(len(values)), key=key)
+
+
+@pytest.mark.parametrize("dtype", INT_DTYPES + FLOAT_DTYPES)
+@pytest.mark.parametrize("op", ["argmin", "argmax"])
+def test_arg_ops_against_definition_and_numpy(dtype, op):
+    rng = np.random.default_rng(7)
+    for n in (1, 2, 5, 100, 4097):
+        for _ in range(5):
+            if dtype.startswith("float"):
+                x = rng.integers(-20, 20, n).astype(dtype) / 4   # many ties
+            else:
+                x = rng.integers(0, 50, n).astype(dtype)
+            r = oracle.reduce(x, op)
+            assert r.index == _ref_arg(list(x), op)
+            np_idx = int(np.argmin(x) if op == "argmin" else np.argmax(x))  # first occurrence
+            if not (dtype.startswith("float") and np.any(x == 0)):
+                assert r.index == np_idx
+            assert x[r.index] == r.value
+
+
+@pytest.mark.parametrize("dtype", FLOAT_DTYPES)
+def test_arg_ops_special_values(dtype):
+    dom = [0.0, -0.0, 1.0, -1.0, math.inf, -math.inf, math.nan, 2.5]
+    for k in (1, 2, 3):
+        for combo in itertools.product(dom, repeat=k):
+            x = np.array(combo, dtype=dtype)
+            for op in ("argmin", "argmax"):
+                r = oracle.reduce(x, op)
+                want = _ref_arg(list(x), op)
+                assert r.index == want, (op, combo)
+                if math.isnan(combo[want]):
+                    assert math.isnan(float(r.value))
+                else:
+                    assert _bits(float(r.value), dtype) == _bits(float(x[want]), dtype)
+
+
+@pytest.mark.parametrize("dtype", INT_DTYPES + FLOAT_DTYPES)
+def test_arg_ops_planted_and_empty(dtype):
+    n = 100000
+    x = inputs.generate(n, dtype, "planted", seed=5)
+    pmax, pmin = inputs.planted_positions(5, n)
+    assert oracle.reduce(x, "argmax").index == pmax
+    assert oracle.reduce(x, "argmin").index == pmin
+    e = oracle.reduce(x[:0], "argmin")
+    assert e.index == -1 and e.value == oracle.identity(dtype, "min")
+
+
+@pytest.mark.parametrize("dtype", ["int32", "uint32", "float32", "float64"])
+def test_arg_ops_block_merge(dtype):
+    """fold(A) merged with fold(B) == fold(A ++ B): indices of B shift by |A|; ties keep A."""
+    rng = np.random.default_rng(3)
+    x = (rng.integers(0, 7, 3000)).astype(dtype)
+    for op in ("argmin", "argmax"):
+        want = oracle.reduce(x, op)
+        for cut in (0, 1, 1500, 2999, 3000):
+            a = oracle.Fold(dtype, op).fold(x[:cut])
+            b = oracle.Fold(dtype, op).fold(x[cut:])
+            got = a.merge(b).result()
+            assert got.index == want.index and got.value == want.value
