@@ -28,6 +28,8 @@
  *    else RD_ERR_MISALIGNED); any element offset is valid.
  *  - Bitwise ops (AND/OR/XOR) on float dtypes -> RD_ERR_UNSUPPORTED.
  *  - n == 0 writes the empty result (table below) and returns RD_OK.
+ *  - For RD_ARGMIN / RD_ARGMAX every `out` below points to an rd_arg_result
+ *    (8-byte aligned) instead of one element.
  *
  * Results:
  *  - integers: + and x wrap modulo 2^w; min/max signed for int32/int64,
@@ -60,7 +62,28 @@ extern "C" {
 #endif
 
 typedef enum { RD_INT32 = 0, RD_UINT32 = 1, RD_INT64 = 2, RD_FLOAT32 = 3, RD_FLOAT64 = 4 } rd_dtype;
-typedef enum { RD_SUM = 0, RD_PROD = 1, RD_MIN = 2, RD_MAX = 3, RD_AND = 4, RD_OR = 5, RD_XOR = 6 } rd_op;
+typedef enum {
+  RD_SUM = 0, RD_PROD = 1, RD_MIN = 2, RD_MAX = 3, RD_AND = 4, RD_OR = 5, RD_XOR = 6,
+  /* (value, smallest index) of the min / max -- the paper's
+   * consumers are shortest paths and golden-section search.
+   * `out` points to an rd_arg_result. NaN anywhere: value NaN, index of the
+   * first NaN; -0.0 ranks below +0.0; empty: identity value, index -1. */
+  RD_ARGMIN = 7, RD_ARGMAX = 8,
+  /* compensated sum (P:50 fn 3, "double precision ... or
+   * ... Kahan"): fp32 accumulates in fp64, fp64 in double-double (TwoSum per
+   * term), so the result is the exact sum rounded once except in near-tie
+   * cases -- in practice independent of order, grid and GPU count.
+   * |result - exact| <= 0.5 ulp(result) + 4 * u_acc * sum|x_i| on the
+   * workloads of DESIGN.md, u_acc = 2^-53 (fp32 data) / 2^-106 (fp64 data).
+   * Integers: identical to RD_SUM. */
+  RD_SUM_COMPENSATED = 9
+} rd_op;
+
+/* Output of RD_ARGMIN / RD_ARGMAX (16 bytes, 8-byte aligned). */
+typedef struct rd_arg_result {
+  uint64_t value;   /* the element's bits in the low sizeof(dtype) bytes (little endian) */
+  int64_t index;    /* smallest index attaining it; -1 for n == 0 */
+} rd_arg_result;
 typedef enum {
   RD_OK = 0,
   RD_ERR_INVALID_ARG = 1,  /* NULL where a buffer is needed, unknown enum, bad config  */
@@ -84,7 +107,9 @@ typedef struct CUstream_st* rd_stream_t;
  *   n      = number of elements the partial covers
  *   acc    = the accumulator bits (integer value; fp32 +: float bits;
  *            fp32 x / fp64 +: double bits; fp64 x: double-double hi, lo;
- *            float min/max: order-preserving key and the max |x| bit pattern)
+ *            float min/max: order-preserving key and the max |x| bit pattern;
+ *            argmin/argmax: order key and the index WITHIN the block, which
+ *            rd_combine_records shifts by the n of the records before it)
  */
 typedef struct rd_record {
   uint32_t tag;
@@ -156,7 +181,8 @@ rd_status rd_comm_check(rd_comm_t comm, rd_stream_t stream);
 rd_status rd_shard_range(uint64_t n, int nranks, int rank, uint64_t* begin, uint64_t* count);
 
 /* ---------------------------------------------------------------- helpers */
-/* Host copy of the empty result (table above) into host_out (one element). */
+/* Host copy of the empty result (table above) into host_out (one element;
+ * an rd_arg_result with index -1 for RD_ARGMIN / RD_ARGMAX). */
 rd_status rd_identity(rd_dtype dtype, rd_op op, void* host_out);
 /* Frees the cached per-(device, stream) workspaces and reduce_host buffers.
  * Must not race with in-flight calls. */

@@ -35,6 +35,10 @@ DEFAULT_WORKLOAD = {
     ("int", "xor"): "uniform_bits",
     ("float", "sum"): "u01", ("float", "prod"): "near_one", ("float", "min"): "planted",
     ("float", "max"): "planted",
+    # argmin / argmax: small value ranges so the extreme value is tied (lowest index wins)
+    ("int", "argmin"): "int_small", ("int", "argmax"): "int_small",
+    ("float", "argmin"): "u01", ("float", "argmax"): "u01",
+    ("int", "sum_compensated"): "uniform_bits", ("float", "sum_compensated"): "normalish",
 }
 
 

@@ -26,7 +26,8 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 # restated codes (not imported from the CUDA package)
 DTYPES = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
-OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "and": 4, "or": 5, "xor": 6, "argmin": 7, "argmax": 8}
+OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "and": 4, "or": 5, "xor": 6, "argmin": 7, "argmax": 8,
+       "sum_compensated": 9}
 NP_DTYPES = {"int32": np.int32, "uint32": np.uint32, "int64": np.int64,
              "float32": np.float32, "float64": np.float64}
 

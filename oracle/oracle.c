@@ -43,7 +43,7 @@
 /* dtype / op / status numbers (restated, see header comment) */
 enum { OR_INT32 = 0, OR_UINT32 = 1, OR_INT64 = 2, OR_FLOAT32 = 3, OR_FLOAT64 = 4 };
 enum { OR_SUM = 0, OR_PROD = 1, OR_MIN = 2, OR_MAX = 3, OR_AND = 4, OR_OR = 5, OR_XOR = 6,
-       OR_ARGMIN = 7, OR_ARGMAX = 8 };
+       OR_ARGMIN = 7, OR_ARGMAX = 8, OR_SUM_COMPENSATED = 9 };
 enum { OR_OK = 0, OR_INVALID = 1, OR_UNSUPPORTED = 2 };
 
 /* Fold state; mirrored by oracle/__init__.py (ctypes). */
@@ -110,7 +110,10 @@ static double ieee_max(double a, double b) {
 static int is_arg(int op) { return op == OR_ARGMIN || op == OR_ARGMAX; }
 
 int or_init(or_state* st, int dtype, int op) {
-  if (!st || dtype < 0 || dtype > 4 || op < 0 || op > 8) return OR_INVALID;
+  if (!st || dtype < 0 || dtype > 4 || op < 0 || op > 9) return OR_INVALID;
+  /* the compensated sum of the library has the same definition as
+   * the sum; this oracle's sum accumulators are already fp64 / double-double */
+  if (op == OR_SUM_COMPENSATED) op = OR_SUM;
   if (is_float(dtype) && op >= OR_AND && !is_arg(op)) return OR_UNSUPPORTED; /* R5 */
   memset(st, 0, sizeof(*st));
   st->dtype = dtype;
@@ -229,7 +232,8 @@ int or_fold(or_state* st, const void* x, uint64_t n) {
 /* Result of an empty fold: Algorithm 1's initial accumulator (R1); argmin /
  * argmax report the min / max identity value (their index is -1). */
 int or_identity(int dtype, int op, void* out) {
-  if (!out || dtype < 0 || dtype > 4 || op < 0 || op > 8) return OR_INVALID;
+  if (!out || dtype < 0 || dtype > 4 || op < 0 || op > 9) return OR_INVALID;
+  if (op == OR_SUM_COMPENSATED) op = OR_SUM;
   if (op == OR_ARGMIN) op = OR_MIN;
   if (op == OR_ARGMAX) op = OR_MAX;
   if (is_float(dtype) && op >= OR_AND) return OR_UNSUPPORTED;

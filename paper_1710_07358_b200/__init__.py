@@ -26,7 +26,9 @@ __all__ = ["reduce", "reduce_partial", "combine_records", "reduce_host", "reduce
            "ReduceError", "OPS", "RECORD_BYTES"]
 
 OPS = {"sum": _lib.RD_SUM, "prod": _lib.RD_PROD, "min": _lib.RD_MIN, "max": _lib.RD_MAX,
-       "and": _lib.RD_AND, "or": _lib.RD_OR, "xor": _lib.RD_XOR}
+       "and": _lib.RD_AND, "or": _lib.RD_OR, "xor": _lib.RD_XOR,
+       "argmin": _lib.RD_ARGMIN, "argmax": _lib.RD_ARGMAX, "sum_compensated": _lib.RD_SUM_COMPENSATED}
+ARG_OPS = ("argmin", "argmax")
 DTYPE_NAMES = {"int32": _lib.RD_INT32, "uint32": _lib.RD_UINT32, "int64": _lib.RD_INT64,
                "float32": _lib.RD_FLOAT32, "float64": _lib.RD_FLOAT64}
 RECORD_BYTES = 32
@@ -64,6 +66,26 @@ def _stream(t, stream):
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _new_out(dtype, device, op):
+    """Result buffer: one element, or a 16-byte rd_arg_result for argmin/argmax."""
+    torch = _torch()
+    if op in ARG_OPS:
+        return torch.empty(2, dtype=torch.int64, device=device)
+    return torch.empty((), dtype=dtype, device=device)
+
+
+def _arg_view(buf, dtype):
+    """rd_arg_result buffer (2 x int64) -> (value 0-d tensor of dtype, index 0-d int64)."""
+    torch = _torch()
+    esz = torch.empty((), dtype=dtype).element_size()
+    value = buf[0:1].view(torch.uint8)[:esz].view(dtype)[0]
+    return value, buf[1]
+
+
+def _result(out, dtype, op):
+    return _arg_view(out, dtype) if op in ARG_OPS else out
+
+
 def _check_input(x):
     if not x.is_cuda:
         raise ValueError("x must be a CUDA tensor (use reduce_host for host arrays)")
@@ -72,14 +94,15 @@ def _check_input(x):
 
 
 def reduce(x, op: str, out=None, stream=None):
-    """x_0 (x) ... (x) x_{n-1} over all elements of the contiguous CUDA tensor x."""
-    torch = _torch()
+    """x_0 (x) ... (x) x_{n-1} over all elements of the contiguous CUDA tensor x.
+    Returns a 0-d tensor; for "argmin"/"argmax" a (value, index) pair of 0-d
+    tensors (views of one 16-byte rd_arg_result; `out` is then 2 x int64)."""
     _check_input(x)
     if out is None:
-        out = torch.empty((), dtype=x.dtype, device=x.device)
+        out = _new_out(x.dtype, x.device, op)
     check(lib().reduce(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
                        out.data_ptr(), _stream(x, stream)), "reduce")
-    return out
+    return _result(out, x.dtype, op)
 
 
 def reduce_partial(x, op: str, rec=None, stream=None):
@@ -101,14 +124,14 @@ def combine_records(recs, dtype, op: str, out=None, rec_out=None, status=None, s
     if recs.numel() % RECORD_BYTES:
         raise ValueError("recs must hold whole 32-byte records")
     if out is None and rec_out is None:
-        out = torch.empty((), dtype=tdt, device=recs.device)
+        out = _new_out(tdt, recs.device, op)
     check(lib().rd_combine_records(recs.data_ptr() if recs.numel() else None, recs.numel() // RECORD_BYTES,
                                    DTYPE_NAMES[name], _op(op),
                                    out.data_ptr() if out is not None else None,
                                    rec_out.data_ptr() if rec_out is not None else None,
                                    status.data_ptr() if status is not None else None,
                                    _stream(recs, stream)), "rd_combine_records")
-    return out if out is not None else rec_out
+    return _result(out, tdt, op) if out is not None else rec_out
 
 
 def reduce_host(x, op: str):
@@ -124,6 +147,12 @@ def reduce_host(x, op: str):
         name, ptr, n = _dtype_name(x.dtype), x.data_ptr(), x.numel()
     if name not in DTYPE_NAMES:
         raise TypeError(f"unsupported dtype {name}")
+    if op in ARG_OPS:
+        r = _lib.rd_arg_result()
+        check(lib().reduce_host(ptr if n else None, n, DTYPE_NAMES[name], _op(op), ctypes.addressof(r)),
+              "reduce_host")
+        v = np.array([r.value], dtype=np.uint64).view(np.uint8)[:np.dtype(name).itemsize].view(np.dtype(name))[0]
+        return v, int(r.index)
     out = np.zeros(1, dtype=np.dtype(name))
     check(lib().reduce_host(ptr if n else None, n, DTYPE_NAMES[name], _op(op), out.ctypes.data),
           "reduce_host")
@@ -134,10 +163,9 @@ def reduce_host(x, op: str):
 def reduce_ex(x, op: str, variant: str = "auto", unroll: int = 0, vec_bytes: int = 0, grid: int = 0,
               out=None, stream=None):
     """reduce with an explicit kernel configuration; returns (out, info dict)."""
-    torch = _torch()
     _check_input(x)
     if out is None:
-        out = torch.empty((), dtype=x.dtype, device=x.device)
+        out = _new_out(x.dtype, x.device, op)
     cfg = _lib.rd_config(VARIANTS[variant], vec_bytes, unroll, 0, grid)
     info = _lib.rd_launch_info()
     check(lib().rd_reduce_ex(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
@@ -145,7 +173,7 @@ def reduce_ex(x, op: str, variant: str = "auto", unroll: int = 0, vec_bytes: int
           "rd_reduce_ex")
     d = {k: getattr(info, k) for k, _ in _lib.rd_launch_info._fields_ if k != "reserved"}
     d["variant"] = {v: k for k, v in VARIANTS.items()}[d["variant"]]
-    return out, d
+    return _result(out, x.dtype, op), d
 
 
 def shard_range(n: int, nranks: int, rank: int):
@@ -156,8 +184,14 @@ def shard_range(n: int, nranks: int, rank: int):
 
 
 def identity(dtype, op: str):
-    """The empty-input result (include/b200reduce.h table) as a numpy scalar."""
+    """The empty-input result (include/b200reduce.h table) as a numpy scalar;
+    (value, -1) for argmin / argmax."""
     name = _dtype_name(dtype)
+    if op in ARG_OPS:
+        r = _lib.rd_arg_result()
+        check(lib().rd_identity(DTYPE_NAMES[name], _op(op), ctypes.addressof(r)), "rd_identity")
+        v = np.array([r.value], dtype=np.uint64).view(np.uint8)[:np.dtype(name).itemsize].view(np.dtype(name))[0]
+        return v, int(r.index)
     out = np.zeros(1, dtype=np.dtype(name))
     check(lib().rd_identity(DTYPE_NAMES[name], _op(op), out.ctypes.data), "rd_identity")
     return out[0]
@@ -218,11 +252,10 @@ class Comm:
 def reduce_multi(x_local, op: str, comm: Comm, out=None, stream=None):
     """Sharded reduce: every rank passes its contiguous block (rank order);
     every rank receives the bitwise-identical result."""
-    torch = _torch()
     _check_input(x_local)
     if out is None:
-        out = torch.empty((), dtype=x_local.dtype, device=x_local.device)
+        out = _new_out(x_local.dtype, x_local.device, op)
     check(lib().reduce_multi(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
                              _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
                              comm.handle), "reduce_multi")
-    return out
+    return _result(out, x_local.dtype, op)

@@ -13,6 +13,7 @@ LIB_PATH = os.path.join(_HERE, "libb200reduce.so")
 
 RD_INT32, RD_UINT32, RD_INT64, RD_FLOAT32, RD_FLOAT64 = range(5)
 RD_SUM, RD_PROD, RD_MIN, RD_MAX, RD_AND, RD_OR, RD_XOR = range(7)
+RD_ARGMIN, RD_ARGMAX, RD_SUM_COMPENSATED = 7, 8, 9
 RD_OK = 0
 STATUS = {0: "RD_OK", 1: "RD_ERR_INVALID_ARG", 2: "RD_ERR_UNSUPPORTED", 3: "RD_ERR_MISALIGNED",
           4: "RD_ERR_CUDA", 5: "RD_ERR_NCCL", 6: "RD_ERR_MISMATCH"}
@@ -22,6 +23,10 @@ RD_VARIANT_AUTO, RD_VARIANT_VECTOR, RD_VARIANT_PAPER, RD_VARIANT_BULK = 0, 1, 2,
 class rd_record(ctypes.Structure):
     _fields_ = [("tag", ctypes.c_uint32), ("status", ctypes.c_uint32), ("n", ctypes.c_uint64),
                 ("acc", ctypes.c_uint64 * 2)]
+
+
+class rd_arg_result(ctypes.Structure):
+    _fields_ = [("value", ctypes.c_uint64), ("index", ctypes.c_int64)]
 
 
 class rd_unique_id(ctypes.Structure):

@@ -28,10 +28,14 @@ int dtype_size(int dtype) {
   return (dtype == RD_INT64 || dtype == RD_FLOAT64) ? 8 : 4;
 }
 
+bool is_arg_op(int op) { return op == RD_ARGMIN || op == RD_ARGMAX; }
+
+int out_size(int dtype, int op) { return is_arg_op(op) ? (int)sizeof(rd_arg_result) : dtype_size(dtype); }
+
 rd_status check_dtype_op(int dtype, int op) {
   if (dtype < RD_INT32 || dtype > RD_FLOAT64) { set_error("unknown dtype"); return RD_ERR_INVALID_ARG; }
-  if (op < RD_SUM || op > RD_XOR) { set_error("unknown op"); return RD_ERR_INVALID_ARG; }
-  if ((dtype == RD_FLOAT32 || dtype == RD_FLOAT64) && op >= RD_AND) {
+  if (op < RD_SUM || op > RD_SUM_COMPENSATED) { set_error("unknown op"); return RD_ERR_INVALID_ARG; }
+  if ((dtype == RD_FLOAT32 || dtype == RD_FLOAT64) && op >= RD_AND && op <= RD_XOR) {
     set_error("bitwise op on a float dtype");
     return RD_ERR_UNSUPPORTED;
   }
@@ -137,7 +141,7 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   if (mode == 0 && out == nullptr) { set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
   if (mode == 1 && rec == nullptr) { set_error("rec is NULL"); return RD_ERR_INVALID_ARG; }
   if ((uintptr_t)x % s != 0) { set_error("x is not aligned to sizeof(dtype)"); return RD_ERR_MISALIGNED; }
-  if (mode == 0 && (uintptr_t)out % s != 0) { set_error("out is not aligned to sizeof(dtype)"); return RD_ERR_MISALIGNED; }
+  if (mode == 0 && (uintptr_t)out % (is_arg_op(op) ? 8 : s) != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
   if (mode == 1 && (uintptr_t)rec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
 
@@ -275,7 +279,7 @@ rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, vo
   if (st != RD_OK) return st;
   if (count < 0 || (count > 0 && recs == nullptr)) { set_error("bad recs/count"); return RD_ERR_INVALID_ARG; }
   if (out == nullptr && rec_out == nullptr) { set_error("no output"); return RD_ERR_INVALID_ARG; }
-  if (out && (uintptr_t)out % dtype_size(dtype)) { set_error("out misaligned"); return RD_ERR_MISALIGNED; }
+  if (out && (uintptr_t)out % (is_arg_op(op) ? 8 : dtype_size(dtype))) { set_error("out misaligned"); return RD_ERR_MISALIGNED; }
   CombineFn fn = lookup_combine(dtype, op);
   if (!fn) { set_error("no combine kernel"); return RD_ERR_UNSUPPORTED; }
   fn<<<1, 32, 0, stream>>>(recs, count, record_tag(dtype, op), out, rec_out, d_status);
@@ -324,6 +328,15 @@ rd_status rd_identity(rd_dtype dtype, rd_op op, void* host_out) {
   rd_status st = rd::check_dtype_op(dtype, op);
   if (st != RD_OK) return st;
   if (!host_out) { rd::set_error("host_out is NULL"); return RD_ERR_INVALID_ARG; }
+  if (rd::is_arg_op(op)) {
+    rd_arg_result r;
+    r.value = 0;
+    r.index = -1;
+    rd_identity(dtype, op == RD_ARGMIN ? RD_MIN : RD_MAX, &r.value);
+    std::memcpy(host_out, &r, sizeof(r));
+    return RD_OK;
+  }
+  if (op == RD_SUM_COMPENSATED) op = RD_SUM;
   if (dtype == RD_FLOAT32 || dtype == RD_FLOAT64) {
     const double inf = __builtin_huge_val();
     double v = op == RD_SUM ? 0.0 : op == RD_PROD ? 1.0 : op == RD_MIN ? inf : -inf;

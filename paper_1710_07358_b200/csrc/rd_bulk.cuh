@@ -73,7 +73,7 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 template <int STAGES, int STAGE_BYTES, int CW>
 struct BulkSmem {
   static constexpr int kRing = STAGES * STAGE_BYTES;
-  static constexpr int kBytes = kRing + 1024;   // ring + barriers + stage metadata + partials
+  static constexpr int kBytes = kRing + 2048;   // ring + barriers + stage metadata + partials (< 1 KB)
 };
 
 template <class OpT, int STAGES, int STAGE_BYTES, int CW>
@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   unsigned char* ring = smem_raw;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  int32_t* st_chunk = reinterpret_cast<int32_t*>(empty + STAGES);
+  uint64_t* st_off = empty + STAGES;                  // body byte offset of each stage
+  int32_t* st_chunk = reinterpret_cast<int32_t*>(st_off + STAGES);
   uint32_t* st_bytes = reinterpret_cast<uint32_t*>(st_chunk + STAGES);
   uint32_t* st_last = st_bytes + STAGES;
   Acc* wpart = reinterpret_cast<Acc*>(reinterpret_cast<uintptr_t>(st_last + STAGES + 3) & ~(uintptr_t)15);  // [2][CW]
@@ -131,6 +132,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
           const uint32_t bytes = (uint32_t)min((uint64_t)STAGE_BYTES, cend - off);
           mbar_wait(&empty[stage], phase ^ 1);
           st_chunk[stage] = (int32_t)c;
+          st_off[stage] = off;
           st_bytes[stage] = bytes;
           st_last[stage] = (off + bytes == cend);
           mbar_arrive_expect_tx(&full[stage], bytes);
@@ -155,6 +157,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
       const uint32_t bytes = st_bytes[stage];
       const uint32_t last = st_last[stage];
       const uint32_t base = ring_addr + stage * STAGE_BYTES;
+      // global element index of this stage's first element (indexed ops only)
+      const uint64_t e0 = OpT::kIndexed ? args.head + st_off[stage] / sizeof(T) : 0;
       if (bytes == STAGE_BYTES) {
         uint4 v[PER_THREAD];
 #pragma unroll
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
         for (int k = 0; k < PER_THREAD; ++k) {
           Vec<16> w{{v[k].x, v[k].y, v[k].z, v[k].w}};
 #pragma unroll
-          for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, 16>(w, l));
+          for (int l = 0; l < L; ++l) acc[l] = fold_at<OpT>(acc[l], lane<T, 16>(w, l), e0 + (k * CT + t) * L + l);
         }
       } else {
 #pragma unroll
@@ -173,7 +177,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
             uint4 q = lds128(base + off);
             Vec<16> w{{q.x, q.y, q.z, q.w}};
 #pragma unroll
-            for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, 16>(w, l));
+            for (int l = 0; l < L; ++l) acc[l] = fold_at<OpT>(acc[l], lane<T, 16>(w, l), e0 + (k * CT + t) * L + l);
           }
         }
       }
@@ -216,9 +220,10 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   if (!s_last) return;
   __threadfence();
   Acc b = fold_slots<OpT, B>(args.partials, args.nchunks);
-  if (threadIdx.x < args.head) b = OpT::fold(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)));
+  if (threadIdx.x < args.head) b = fold_at<OpT>(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)), threadIdx.x);
   if (threadIdx.x < args.tail)
-    b = OpT::fold(b, ldg_scalar<T>(args.x + (args.tail_start + threadIdx.x) * sizeof(T)));
+    b = fold_at<OpT>(b, ldg_scalar<T>(args.x + (args.tail_start + threadIdx.x) * sizeof(T)),
+                     args.tail_start + threadIdx.x);
   b = block_reduce<OpT, B>(b, red);
   if (threadIdx.x == 0) {
     finish<OpT>(b, args);

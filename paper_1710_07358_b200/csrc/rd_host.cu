@@ -125,7 +125,7 @@ extern "C" rd_status reduce_host(const void* x_host, size_t n, rd_dtype dtype, r
   }
   st = launch_combine(p->recs, (int)nchunks, dtype, op, p->d_out, nullptr, nullptr, p->comp);
   if (st != RD_OK) return st;
-  if ((e = cudaMemcpyAsync(out_host, p->d_out, s, cudaMemcpyDeviceToHost, p->comp)) != cudaSuccess)
+  if ((e = cudaMemcpyAsync(out_host, p->d_out, out_size(dtype, op), cudaMemcpyDeviceToHost, p->comp)) != cudaSuccess)
     return cuda_fail(e, "D2H copy");
   if ((e = cudaStreamSynchronize(p->comp)) != cudaSuccess) return cuda_fail(e, "synchronize");
   return RD_OK;

@@ -15,6 +15,8 @@ bool lookup_int(int dtype, int op, int variant, int unroll, int vec_bytes, Kerne
       RD_CASE_DEFAULT(DT, RD_MIN) RD_CASE_DEFAULT(DT, RD_MAX)                   \
       RD_CASE_DEFAULT(DT, RD_AND) RD_CASE_DEFAULT(DT, RD_OR)                    \
       RD_CASE_DEFAULT(DT, RD_XOR)                                               \
+      RD_CASE_DEFAULT(DT, RD_ARGMIN) RD_CASE_DEFAULT(DT, RD_ARGMAX)             \
+      RD_CASE_DEFAULT(DT, RD_SUM_COMPENSATED)                                   \
       default: return false;                                                    \
     }
   switch (dtype) {
@@ -32,6 +34,8 @@ bool lookup_float(int dtype, int op, int variant, int unroll, int vec_bytes, Ker
     switch (op) {                                                               \
       RD_CASE_DEFAULT(DT, RD_SUM) RD_CASE_DEFAULT(DT, RD_PROD)                  \
       RD_CASE_DEFAULT(DT, RD_MIN) RD_CASE_DEFAULT(DT, RD_MAX)                   \
+      RD_CASE_DEFAULT(DT, RD_ARGMIN) RD_CASE_DEFAULT(DT, RD_ARGMAX)             \
+      RD_CASE_DEFAULT(DT, RD_SUM_COMPENSATED)                                   \
       default: return false;                                                    \
     }
   switch (dtype) {
@@ -46,8 +50,10 @@ CombineFn lookup_combine(int dtype, int op) {
 #define RD_C(DT, OP) \
   if (dtype == DT && op == OP) return rd_combine_kernel<typename OpFor<DT, OP>::type>;
 #define RD_C_INT(DT) RD_C(DT, RD_SUM) RD_C(DT, RD_PROD) RD_C(DT, RD_MIN) RD_C(DT, RD_MAX) \
-  RD_C(DT, RD_AND) RD_C(DT, RD_OR) RD_C(DT, RD_XOR)
-#define RD_C_FLT(DT) RD_C(DT, RD_SUM) RD_C(DT, RD_PROD) RD_C(DT, RD_MIN) RD_C(DT, RD_MAX)
+  RD_C(DT, RD_AND) RD_C(DT, RD_OR) RD_C(DT, RD_XOR) RD_C(DT, RD_ARGMIN) RD_C(DT, RD_ARGMAX)   \
+  RD_C(DT, RD_SUM_COMPENSATED)
+#define RD_C_FLT(DT) RD_C(DT, RD_SUM) RD_C(DT, RD_PROD) RD_C(DT, RD_MIN) RD_C(DT, RD_MAX) \
+  RD_C(DT, RD_ARGMIN) RD_C(DT, RD_ARGMAX) RD_C(DT, RD_SUM_COMPENSATED)
   RD_C_INT(RD_INT32) RD_C_INT(RD_UINT32) RD_C_INT(RD_INT64)
   RD_C_FLT(RD_FLOAT32) RD_C_FLT(RD_FLOAT64)
 #undef RD_C_FLT

@@ -16,6 +16,8 @@ rd_status cuda_fail(cudaError_t e, const char* what);
 // argument checks shared by every entry point (synchronous, enqueue nothing)
 rd_status check_dtype_op(int dtype, int op);
 int dtype_size(int dtype);
+bool is_arg_op(int op);
+int out_size(int dtype, int op);   // bytes of one result: element, or rd_arg_result
 
 // Plan + launch one reduction of x[0..n) (a0-a7). mode 0 writes one element
 // to `out`, mode 1 writes one rd_record to `rec`.

@@ -34,7 +34,7 @@ struct KArgs {
   uint64_t nvec;            // VB-byte vectors in the body
   uint64_t tail_start;      // first element after the body
   uint64_t tail;            // elements after the body
-  void* out;                // mode 0: one element of T
+  void* out;                // mode 0: one element of T (rd_arg_result for arg ops)
   rd_record* rec;           // mode 1: one record
   Slot* partials;           // gridDim.x slots (workspace)
   unsigned* ticket;         // zero between launches (workspace)
@@ -223,17 +223,20 @@ __global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, VB>(v[u], l));
+        for (int l = 0; l < L; ++l)
+          acc[l] = fold_at<OpT>(acc[l], lane<T, VB>(v[u], l), args.head + (i + (uint64_t)u * stride) * L + l);
     }
   }
   for (; i < nvec; i += stride) {
     Vec<VB> v = ldg_stream<VB>(body + i * VB);
 #pragma unroll
-    for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], lane<T, VB>(v, l));
+    for (int l = 0; l < L; ++l) acc[l] = fold_at<OpT>(acc[l], lane<T, VB>(v, l), args.head + i * L + l);
   }
   // a2: head and tail stragglers
-  if (tid < args.head) acc[0] = OpT::fold(acc[0], ldg_scalar<T>(args.x + tid * sizeof(T)));
-  if (tid < args.tail) acc[L - 1] = OpT::fold(acc[L - 1], ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T)));
+  if (tid < args.head) acc[0] = fold_at<OpT>(acc[0], ldg_scalar<T>(args.x + tid * sizeof(T)), tid);
+  if (tid < args.tail)
+    acc[L - 1] = fold_at<OpT>(acc[L - 1], ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T)),
+                              args.tail_start + tid);
   pdl_trigger();
   // a3
   Acc a = acc[0];
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(B) rd_paper_kernel(const KArgs args) {
     for (int k = 0; k < F; ++k) v[k] = (pos + k < n) ? __ldg(x + pos + k) : T{};
 #pragma unroll
     for (int k = 0; k < F; ++k)
-      if (pos + k < n) acc = OpT::fold(acc, v[k]);
+      if (pos + k < n) acc = fold_at<OpT>(acc, v[k], pos + k);
   }
   acc = block_reduce<OpT, B>(acc, smem);
   __syncthreads();
@@ -289,8 +292,9 @@ __global__ void rd_combine_kernel(const rd_record* recs, int count, uint32_t tag
   for (int r = 0; r < count; ++r) {
     const rd_record rc = recs[r];
     if (rc.tag != tag) { bad = true; continue; }
+    // record r covers the block after the previous ones: indices shift by n so far
+    a = OpT::combine(a, shifted<OpT>(OpT::unpack(Slot{rc.acc[0], rc.acc[1]}), n));
     n += rc.n;
-    a = OpT::combine(a, OpT::unpack(Slot{rc.acc[0], rc.acc[1]}));
   }
   if (bad && d_status) *d_status = (int)RD_ERR_MISMATCH;
   if (out) {

@@ -87,7 +87,7 @@ rd_status reduce_multi(const void* x_local, size_t n_local, rd_dtype dtype, rd_o
   if (!out) { rd::set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
   rd_status st = rd::check_dtype_op(dtype, op);
   if (st != RD_OK) return st;
-  if ((uintptr_t)out % rd::dtype_size(dtype)) { rd::set_error("out misaligned"); return RD_ERR_MISALIGNED; }
+  if ((uintptr_t)out % (rd::is_arg_op(op) ? 8 : rd::dtype_size(dtype))) { rd::set_error("out misaligned"); return RD_ERR_MISALIGNED; }
   cudaStream_t s = (cudaStream_t)stream;
   // a0-a7 on the local shard -> this rank's record
   st = rd::launch_reduce(x_local, n_local, dtype, op, 1, nullptr, comm->d_send, s, nullptr, nullptr);

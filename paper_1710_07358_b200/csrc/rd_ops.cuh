@@ -41,6 +41,7 @@ struct IntOp {
   using T = U;
   using Acc = U;
   static constexpr bool kFloat = false;
+  static constexpr bool kIndexed = false;
   using S = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
 
   __device__ __forceinline__ static Acc identity() {
@@ -96,6 +97,7 @@ struct FloatSum {
   using T = F;
   using Acc = F;
   static constexpr bool kFloat = true;
+  static constexpr bool kIndexed = false;
   __device__ __forceinline__ static Acc identity() { return (F)(-0.0); }
   __device__ __forceinline__ static Acc combine(Acc a, Acc b) { return a + b; }
   __device__ __forceinline__ static Acc fold(Acc a, T x) { return a + x; }
@@ -124,6 +126,7 @@ struct Float32Prod {
   using T = float;
   using Acc = double;
   static constexpr bool kFloat = true;
+  static constexpr bool kIndexed = false;
   __device__ __forceinline__ static Acc identity() { return 1.0; }
   __device__ __forceinline__ static Acc combine(Acc a, Acc b) { return __dmul_rn(a, b); }
   __device__ __forceinline__ static Acc fold(Acc a, T x) { return __dmul_rn(a, (double)x); }
@@ -152,6 +155,7 @@ struct Float64Prod {
   using T = double;
   using Acc = DD;
   static constexpr bool kFloat = true;
+  static constexpr bool kIndexed = false;
   __device__ __forceinline__ static Acc identity() { return DD{1.0, 0.0}; }
   __device__ __forceinline__ static Acc fold(Acc a, T x) {
     const double p = __dmul_rn(a.hi, x);
@@ -202,6 +206,7 @@ struct FloatMinMax {
   using S = typename std::conditional<sizeof(F) == 4, int32_t, int64_t>::type;
   struct Acc { S key; U amax; };
   static constexpr bool kFloat = true;
+  static constexpr bool kIndexed = false;
   static constexpr U kAbsMask = (U)(~(U)0) >> 1;
   static constexpr U kInfBits = sizeof(F) == 4 ? (U)0x7f800000u : (U)0x7ff0000000000000ull;
 
@@ -249,6 +254,165 @@ struct FloatMinMax {
   __device__ __forceinline__ static Acc unpack(Slot s) { return Acc{(S)(U)s.a, (U)s.b}; }
 };
 
+// ------------------------------------------- compensated float + 
+// fp32: fp64 accumulator (every fp32 term exact in fp64); fp64: double-double
+// with an error-free TwoSum per term (6 DP ops), lo not renormalised (its own
+// error stays ~n u^2 sum|x|). The result is the exact sum rounded once in all
+// but near-tie cases, hence (in practice) independent of the evaluation order,
+// the grid and the number of GPUs (P:50 fn 3: "strategies to reduce truncation
+// errors, like the one proposed by Kahan").
+struct Float32SumComp {
+  using T = float;
+  using Acc = double;
+  static constexpr bool kFloat = true;
+  static constexpr bool kIndexed = false;
+  __device__ __forceinline__ static Acc identity() { return -0.0; }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) { return __dadd_rn(a, b); }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) { return __dadd_rn(a, (double)x); }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) a = __dadd_rn(a, shfl_xor_f64(a, m));
+    return a;
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) { *(float*)out = __double2float_rn(a); }
+  __device__ __forceinline__ static void store_empty(void* out) { *(float*)out = 0.0f; }
+  __device__ __forceinline__ static Slot pack(Acc a) { return Slot{(uint64_t)__double_as_longlong(a), 0}; }
+  __device__ __forceinline__ static Acc unpack(Slot s) { return __longlong_as_double((long long)s.a); }
+};
+
+struct Float64SumComp {
+  using T = double;
+  using Acc = DD;
+  static constexpr bool kFloat = true;
+  static constexpr bool kIndexed = false;
+  __device__ __forceinline__ static Acc identity() { return DD{-0.0, -0.0}; }
+  // TwoSum (Knuth): s + e == a + b exactly
+  __device__ __forceinline__ static Acc two_sum_into(double hi, double lo, double x) {
+    const double s = __dadd_rn(hi, x);
+    const double bp = __dsub_rn(s, hi);
+    const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bp)), __dsub_rn(x, bp));
+    return DD{s, __dadd_rn(lo, e)};
+  }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) { return two_sum_into(a.hi, a.lo, x); }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) {
+    Acc r = two_sum_into(a.hi, a.lo, b.hi);
+    r.lo = __dadd_rn(r.lo, b.lo);
+    return r;
+  }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      DD o{shfl_xor_f64(a.hi, m), shfl_xor_f64(a.lo, m)};
+      a = combine(a, o);
+    }
+    return a;
+  }
+  __device__ __forceinline__ static double value(Acc a) {
+    // non-finite: the plain sum decides (TwoSum's error term is NaN there);
+    // lo == 0 keeps the sign of a zero sum (-0.0 iff every term is -0.0)
+    if (!(fabs(a.hi) < __longlong_as_double(0x7ff0000000000000LL))) return a.hi;
+    return a.lo == 0.0 ? a.hi : __dadd_rn(a.hi, a.lo);
+  }
+  __device__ __forceinline__ static void store(Acc a, void* out) { *(double*)out = value(a); }
+  __device__ __forceinline__ static void store_empty(void* out) { *(double*)out = 0.0; }
+  __device__ __forceinline__ static Slot pack(Acc a) {
+    return Slot{(uint64_t)__double_as_longlong(a.hi), (uint64_t)__double_as_longlong(a.lo)};
+  }
+  __device__ __forceinline__ static Acc unpack(Slot s) {
+    return DD{__longlong_as_double((long long)s.a), __longlong_as_double((long long)s.b)};
+  }
+};
+
+// ------------------------------------------------- argmin / argmax
+// Value and the SMALLEST index attaining it (reading R6). Every element maps
+// to an unsigned order key K (ints: sign-flipped bits; floats: the total-order
+// key of FloatMinMax, with any NaN mapped to the winning end), and (K, index)
+// is compared lexicographically -- exactly associative and commutative, so
+// any evaluation order gives the same (value, index).
+template <typename U, rd_dtype DT, rd_op OP>
+struct ArgOp {
+  using T = U;
+  struct Acc { U key; uint64_t idx; };
+  static constexpr bool kFloat = (DT == RD_FLOAT32 || DT == RD_FLOAT64);
+  static constexpr bool kIndexed = true;
+  static constexpr int kBits = 8 * sizeof(U);
+  static constexpr U kSign = (U)1 << (kBits - 1);
+  static constexpr U kAbs = kSign - 1;
+  static constexpr U kInf = sizeof(U) == 4 ? (U)0x7f800000u : (U)0x7ff0000000000000ull;
+
+  __device__ __forceinline__ static U key_of(U b) {
+    if constexpr (DT == RD_UINT32) return b;
+    else if constexpr (!kFloat) return b ^ kSign;
+    else {
+      if ((b & kAbs) > kInf) return OP == RD_ARGMIN ? (U)0 : (U)~(U)0;   // NaN wins
+      const U skey = b ^ ((U)((typename std::make_signed<U>::type)b >> (kBits - 1)) & kAbs);
+      return skey ^ kSign;
+    }
+  }
+  __device__ __forceinline__ static U bits_of(U k) {   // inverse of key_of (non-NaN)
+    if constexpr (DT == RD_UINT32) return k;
+    else if constexpr (!kFloat) return k ^ kSign;
+    else {
+      if (k == (OP == RD_ARGMIN ? (U)0 : (U)~(U)0)) return kInf | ((U)1 << (sizeof(U) == 4 ? 22 : 51));
+      const U skey = k ^ kSign;
+      return skey ^ ((U)((typename std::make_signed<U>::type)skey >> (kBits - 1)) & kAbs);
+    }
+  }
+  __device__ __forceinline__ static Acc identity() {
+    return OP == RD_ARGMIN ? Acc{(U)~(U)0, ~0ull} : Acc{(U)0, ~0ull};
+  }
+  __device__ __forceinline__ static bool better(const Acc& a, const Acc& b) {   // a strictly before b
+    if (a.key != b.key) return OP == RD_ARGMIN ? a.key < b.key : a.key > b.key;
+    return a.idx < b.idx;
+  }
+  __device__ __forceinline__ static Acc combine(Acc a, Acc b) { return better(b, a) ? b : a; }
+  __device__ __forceinline__ static Acc fold_idx(Acc a, T x, uint64_t i) { return combine(a, Acc{key_of(x), i}); }
+  __device__ __forceinline__ static Acc fold(Acc a, T x) { return fold_idx(a, x, 0); }
+  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      Acc o;
+      if constexpr (sizeof(U) == 4) o.key = __shfl_xor_sync(0xffffffffu, a.key, m);
+      else o.key = (U)shfl_xor_u64((uint64_t)a.key, m);
+      o.idx = shfl_xor_u64(a.idx, m);
+      a = combine(a, o);
+    }
+    return a;
+  }
+  // out -> rd_arg_result {value bits (low sizeof(T) bytes), int64 index}
+  __device__ __forceinline__ static void store(Acc a, void* out) {
+    uint64_t* r = (uint64_t*)out;
+    r[0] = (uint64_t)bits_of(a.key);
+    r[1] = a.idx;
+  }
+  __device__ __forceinline__ static void store_empty(void* out) {
+    uint64_t* r = (uint64_t*)out;
+    U v;
+    if constexpr (kFloat) v = OP == RD_ARGMIN ? kInf : (kInf | kSign);
+    else if constexpr (DT == RD_UINT32) v = OP == RD_ARGMIN ? (U)~(U)0 : (U)0;
+    else v = OP == RD_ARGMIN ? kAbs : kSign;
+    r[0] = (uint64_t)v;
+    r[1] = ~0ull;   // index -1
+  }
+  __device__ __forceinline__ static Slot pack(Acc a) { return Slot{(uint64_t)a.key, a.idx}; }
+  __device__ __forceinline__ static Acc unpack(Slot s) { return Acc{(U)s.a, s.b}; }
+};
+
+// fold with the element's global index (indexed ops), else plain fold
+template <class OpT>
+__device__ __forceinline__ typename OpT::Acc fold_at(typename OpT::Acc a, typename OpT::T x, uint64_t i) {
+  if constexpr (OpT::kIndexed) return OpT::fold_idx(a, x, i);
+  else return OpT::fold(a, x);
+}
+// partial of a later block: indices shift by the elements before it
+template <class OpT>
+__device__ __forceinline__ typename OpT::Acc shifted(typename OpT::Acc a, uint64_t off) {
+  if constexpr (OpT::kIndexed) {
+    if (a.idx != ~0ull) a.idx += off;
+  }
+  return a;
+}
+
 // ---------------------------------------------------------------- type map
 template <rd_dtype DT, rd_op OP> struct OpFor;
 #define RD_INT_OPS(DT, U, SIGNED)                                                  \
@@ -263,6 +427,21 @@ RD_INT_OPS(RD_INT32, uint32_t, true)
 RD_INT_OPS(RD_UINT32, uint32_t, false)
 RD_INT_OPS(RD_INT64, uint64_t, true)
 #undef RD_INT_OPS
+#define RD_ARG_OPS(DT, U)                                                              \
+  template <> struct OpFor<DT, RD_ARGMIN> { using type = ArgOp<U, DT, RD_ARGMIN>; }; \
+  template <> struct OpFor<DT, RD_ARGMAX> { using type = ArgOp<U, DT, RD_ARGMAX>; };
+RD_ARG_OPS(RD_INT32, uint32_t)
+RD_ARG_OPS(RD_UINT32, uint32_t)
+RD_ARG_OPS(RD_INT64, uint64_t)
+RD_ARG_OPS(RD_FLOAT32, uint32_t)
+RD_ARG_OPS(RD_FLOAT64, uint64_t)
+#undef RD_ARG_OPS
+// compensated sum: exact already for integers
+template <> struct OpFor<RD_INT32, RD_SUM_COMPENSATED> { using type = IntOp<uint32_t, RD_SUM, true>; };
+template <> struct OpFor<RD_UINT32, RD_SUM_COMPENSATED> { using type = IntOp<uint32_t, RD_SUM, false>; };
+template <> struct OpFor<RD_INT64, RD_SUM_COMPENSATED> { using type = IntOp<uint64_t, RD_SUM, true>; };
+template <> struct OpFor<RD_FLOAT32, RD_SUM_COMPENSATED> { using type = Float32SumComp; };
+template <> struct OpFor<RD_FLOAT64, RD_SUM_COMPENSATED> { using type = Float64SumComp; };
 template <> struct OpFor<RD_FLOAT32, RD_SUM> { using type = FloatSum<float>; };
 template <> struct OpFor<RD_FLOAT64, RD_SUM> { using type = FloatSum<double>; };
 template <> struct OpFor<RD_FLOAT32, RD_PROD> { using type = Float32Prod; };

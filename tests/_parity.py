@@ -16,6 +16,8 @@ import numpy as np
 import oracle
 
 EPS = {"float32": 2.0 ** -23, "float64": 2.0 ** -52}
+# unit roundoff of the compensated-sum accumulators (fp64 for fp32 data, double-double for fp64)
+U_ACC = {"float32": 2.0 ** -53, "float64": 2.0 ** -106}
 
 
 def to_bits(v, dtype):
@@ -23,9 +25,19 @@ def to_bits(v, dtype):
 
 
 def check(got, x: np.ndarray, op: str, ref=None, factor: float = 4.0):
-    """Assert parity of `got` (numpy scalar / python number) with the oracle on x."""
+    """Assert parity of `got` (numpy scalar / python number; (value, index) for
+    argmin / argmax) with the oracle on x."""
     dtype = x.dtype.name
     r = ref if ref is not None else oracle.reduce(x, op)
+    if op in ("argmin", "argmax"):
+        gv, gi = got
+        assert int(gi) == r.index, f"{dtype} {op} n={x.size}: index {int(gi)} want {r.index}"
+        g = np.array([gv], dtype=x.dtype)[0]
+        if dtype.startswith("float") and math.isnan(float(r.value)):
+            assert math.isnan(float(g))
+        else:
+            assert to_bits(g, dtype) == to_bits(r.value, dtype), f"{op}: value {g!r} want {r.value!r}"
+        return r
     g = np.array([got], dtype=x.dtype)[0]
     if not dtype.startswith("float") or op in ("min", "max"):
         if dtype.startswith("float") and math.isnan(float(r.value)):
@@ -42,11 +54,13 @@ def check(got, x: np.ndarray, op: str, ref=None, factor: float = 4.0):
         else:
             assert gv == want, f"want {want} got {gv}"
         return r
-    if op == "sum":
+    if op in ("sum", "sum_compensated"):
         if r.sum_abs == 0.0:
             assert to_bits(g, dtype) == to_bits(r.value, dtype), f"signed zero: got {gv!r} want {want!r}"
             return r
         tol = factor * EPS[dtype] * r.sum_abs
+        if op == "sum_compensated":   # include/b200reduce.h: 1/2 ulp + 4 u_acc sum|x|
+            tol = 0.5 * float(np.spacing(np.abs(g))) + factor * U_ACC[dtype] * r.sum_abs
     else:
         tol = factor * EPS[dtype] * abs(r.exact)
     err = abs(gv - r.exact)

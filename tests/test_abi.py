@@ -69,6 +69,11 @@ def test_identity_matches_oracle(dtype, op):
             rd.identity(dtype, op)
         assert e.value.status == 2
         return
+    if op in rd.ARG_OPS:
+        v, i = rd.identity(dtype, op)
+        assert i == -1 and v.tobytes() == oracle.identity(dtype, op).tobytes()
+        assert oracle.reduce(np.zeros(0, dtype), op).index == -1
+        return
     a = rd.identity(dtype, op)
     b = oracle.identity(dtype, op)
     assert a.tobytes() == b.tobytes()
@@ -85,7 +90,8 @@ def test_validation_before_any_device_work():
     assert L.reduce(None, 5, 0, 0, out, None) == 1                 # x NULL, n > 0
     assert L.reduce(p, 5, 0, 0, None, None) == 1                   # out NULL
     assert L.reduce(p, 5, 9, 0, out, None) == 1                    # unknown dtype
-    assert L.reduce(p, 5, 0, 9, out, None) == 1                    # unknown op
+    assert L.reduce(p, 5, 0, 10, out, None) == 1                   # unknown op
+    assert L.reduce(p, 5, 0, 7, ctypes.c_void_p(p + 4), None) == 3  # argmin result not 8-aligned
     for op in (4, 5, 6):
         assert L.reduce(p, 5, 3, op, out, None) == 2               # bitwise on float32
         assert L.reduce(p, 5, 4, op, out, None) == 2               # bitwise on float64

@@ -19,7 +19,8 @@ INT = ["int32", "uint32", "int64"]
 FLT = ["float32", "float64"]
 INT_OPS = ["sum", "prod", "min", "max", "and", "or", "xor"]
 FLT_OPS = ["sum", "prod", "min", "max"]
-PAIRS = [(d, o) for d in INT for o in INT_OPS] + [(d, o) for d in FLT for o in FLT_OPS]
+EXTRA_OPS = ["argmin", "argmax", "sum_compensated"]
+PAIRS = [(d, o) for d in INT for o in INT_OPS + EXTRA_OPS] + [(d, o) for d in FLT for o in FLT_OPS + EXTRA_OPS]
 SIZES = [0, 1, 2, 3, 7, 8, 9, 31, 32, 33, 255, 256, 257, 1023, 1025, 4097, 65535, 65537,
          (1 << 20) + 1, 5533214]
 
@@ -43,7 +44,10 @@ def to_dev(x: np.ndarray, offset: int = 0):
 
 
 def val(t):
-    """0-d CUDA tensor -> numpy scalar of the same dtype (bit-preserving)."""
+    """0-d CUDA tensor -> numpy scalar of the same dtype (bit-preserving);
+    a (value, index) pair -> (numpy scalar, int)."""
+    if isinstance(t, tuple):
+        return val(t[0]), int(t[1].item())
     carrier = {4: torch.int32, 8: torch.int64}[t.element_size()]
     npdt = np.dtype(str(t.dtype).replace("torch.", ""))
     return np.array([t.view(carrier).item()], dtype=np.dtype(str(carrier).replace("torch.", ""))).view(npdt)[0]
@@ -446,3 +450,84 @@ def test_c5_sharded_layout_on_one_gpu(rd):
         _parity.check(g, xh, op)
         if op == "max":
             assert float(g) == 2.0 ** 20
+
+
+# ------------------------------------------------------------------ f4: argmin / argmax
+@pytest.mark.parametrize("prec", FLT)
+def test_arg_ops_special_values(rd, prec):
+    """Reading R6: NaN first (index of the first NaN), -0 < +0, lowest index on ties,
+    in head, body and tail positions, for both kernel variants."""
+    import itertools
+    dom = [0.0, -0.0, 1.0, -1.0, math.inf, -math.inf, math.nan, 2.5]
+    for k in (1, 2, 3):
+        for combo in itertools.product(dom, repeat=k):
+            x = np.array(combo, dtype=prec)
+            for op in ("argmin", "argmax"):
+                _parity.check(val(rd.reduce(to_dev(x, 1), op)), x, op)
+    base = np.full(100003, 7.0, dtype=prec)
+    for v in dom:
+        for pos in (0, 3, 777, 50000, 100002):
+            x = base.copy()
+            x[pos] = v
+            x[(pos * 7 + 13) % x.size] = v          # a tie later (or earlier) in the array
+            for op in ("argmin", "argmax"):
+                for variant in ("vector", "bulk"):
+                    got = val(rd.reduce_ex(to_dev(x, pos % 4), op, variant=variant)[0])
+                    _parity.check(got, x, op)
+
+
+@pytest.mark.parametrize("dtype", INT + FLT)
+def test_arg_ops_sharded_records(rd, dtype):
+    """Shard records carry block-local indices; rd_combine_records shifts them by
+    the elements of the records before (rank order) -> global index."""
+    n = (1 << 22) + 9
+    for op in ("argmin", "argmax"):
+        x = inputs.generate(n, dtype, inputs.default_workload(dtype, op), seed=2)
+        xd = to_dev(x)
+        for W in (1, 2, 5, 8):
+            recs = torch.empty(W * 32, dtype=torch.uint8, device="cuda")
+            for r in range(W):
+                b, c = rd.shard_range(n, W, r)
+                rd.reduce_partial(xd[b:b + c], op, rec=recs[r * 32:(r + 1) * 32])
+            _parity.check(val(rd.combine_records(recs, dtype, op)), x, op)
+
+
+def test_arg_ops_full_size(rd):
+    """2^28 float32 with the planted extremes: the planted indices come back."""
+    n = 1 << 28
+    x = _device_input(n, "float32", "planted", 4)
+    pmax, pmin = inputs.planted_positions(4, n)
+    v, i = val(rd.reduce(x, "argmax"))
+    assert (float(v), i) == (2.0 ** 20, pmax)
+    v, i = val(rd.reduce(x, "argmin"))
+    assert (float(v), i) == (-(2.0 ** 20), pmin)
+    xh = x.cpu().numpy()
+    del x
+    xd = _device_input(n, "float32", "u01", 5)   # 2^24-point grid: the extremes are tied
+    for op in ("argmin", "argmax"):
+        _parity.check(val(rd.reduce(xd, op)), xd.cpu().numpy(), op)
+    del xh
+
+
+# ------------------------------------------------------------------ f2: compensated sum
+@pytest.mark.parametrize("dtype", FLT)
+@pytest.mark.parametrize("wl", ["u01", "normalish"])
+def test_compensated_sum_full_size(rd, dtype, wl):
+    """n = 2^28: within 1/2 ulp + 4 u_acc sum|x| of the exact sum, and equal to the
+    oracle's correctly rounded value; identical bits across kernel variants, grids
+    and a sharded evaluation (reproducible in practice)."""
+    n = 1 << 28
+    x = _device_input(n, dtype, wl, 1)
+    g = val(rd.reduce(x, "sum_compensated"))
+    variants = {val(rd.reduce_ex(x, "sum_compensated", variant=v, grid=gr)[0]).tobytes()
+                for v, gr in (("vector", 0), ("vector", 1000), ("bulk", 0), ("bulk", 37))}
+    recs = torch.empty(8 * 32, dtype=torch.uint8, device="cuda")
+    for r in range(8):
+        b, c = rd.shard_range(n, 8, r)
+        rd.reduce_partial(x[b:b + c], "sum_compensated", rec=recs[r * 32:(r + 1) * 32])
+    variants.add(val(rd.combine_records(recs, dtype, "sum_compensated")).tobytes())
+    xh = x.cpu().numpy()
+    del x
+    ref = _parity.check(g, xh, "sum_compensated")
+    assert g.tobytes() == np.array([ref.value]).astype(dtype).tobytes()
+    assert variants == {g.tobytes()}

@@ -143,7 +143,8 @@ def do_ablation(args):
 def do_ops(args):
     rows = []
     pairs = [(d, o) for d in ("int32", "uint32", "int64") for o in rd.OPS] + \
-            [(d, o) for d in ("float32", "float64") for o in ("sum", "prod", "min", "max")]
+            [(d, o) for d in ("float32", "float64")
+             for o in ("sum", "prod", "min", "max", "argmin", "argmax", "sum_compensated")]
     for log2n in args.log2n:
         n = 1 << log2n
         for dtype, op in pairs:
