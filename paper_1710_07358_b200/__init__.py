@@ -74,6 +74,16 @@ def _new_out(dtype, device, op):
     return torch.empty((), dtype=dtype, device=device)
 
 
+def _check_out(out, dtype, op):
+    """The result buffer must be large enough for what the C call writes."""
+    if op in ARG_OPS:
+        if out.numel() * out.element_size() < 16 or not out.is_contiguous():
+            raise ValueError("argmin/argmax need a 16-byte rd_arg_result buffer (e.g. 2 x int64)")
+    elif out.dtype != dtype:
+        raise ValueError(f"out has dtype {out.dtype}, expected {dtype}")
+    return out
+
+
 def _arg_view(buf, dtype):
     """rd_arg_result buffer (2 x int64) -> (value 0-d tensor of dtype, index 0-d int64)."""
     torch = _torch()
@@ -98,8 +108,7 @@ def reduce(x, op: str, out=None, stream=None):
     Returns a 0-d tensor; for "argmin"/"argmax" a (value, index) pair of 0-d
     tensors (views of one 16-byte rd_arg_result; `out` is then 2 x int64)."""
     _check_input(x)
-    if out is None:
-        out = _new_out(x.dtype, x.device, op)
+    out = _new_out(x.dtype, x.device, op) if out is None else _check_out(out, x.dtype, op)
     check(lib().reduce(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
                        out.data_ptr(), _stream(x, stream)), "reduce")
     return _result(out, x.dtype, op)
@@ -125,6 +134,8 @@ def combine_records(recs, dtype, op: str, out=None, rec_out=None, status=None, s
         raise ValueError("recs must hold whole 32-byte records")
     if out is None and rec_out is None:
         out = _new_out(tdt, recs.device, op)
+    elif out is not None:
+        _check_out(out, tdt, op)
     check(lib().rd_combine_records(recs.data_ptr() if recs.numel() else None, recs.numel() // RECORD_BYTES,
                                    DTYPE_NAMES[name], _op(op),
                                    out.data_ptr() if out is not None else None,
@@ -164,8 +175,7 @@ def reduce_ex(x, op: str, variant: str = "auto", unroll: int = 0, vec_bytes: int
               out=None, stream=None):
     """reduce with an explicit kernel configuration; returns (out, info dict)."""
     _check_input(x)
-    if out is None:
-        out = _new_out(x.dtype, x.device, op)
+    out = _new_out(x.dtype, x.device, op) if out is None else _check_out(out, x.dtype, op)
     cfg = _lib.rd_config(VARIANTS[variant], vec_bytes, unroll, 0, grid)
     info = _lib.rd_launch_info()
     check(lib().rd_reduce_ex(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
@@ -253,8 +263,7 @@ def reduce_multi(x_local, op: str, comm: Comm, out=None, stream=None):
     """Sharded reduce: every rank passes its contiguous block (rank order);
     every rank receives the bitwise-identical result."""
     _check_input(x_local)
-    if out is None:
-        out = _new_out(x_local.dtype, x_local.device, op)
+    out = _new_out(x_local.dtype, x_local.device, op) if out is None else _check_out(out, x_local.dtype, op)
     check(lib().reduce_multi(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
                              _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
                              comm.handle), "reduce_multi")

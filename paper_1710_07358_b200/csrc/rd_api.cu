@@ -148,9 +148,8 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
   const int unroll = cfg ? cfg->unroll : 0;
   const int vec_bytes = cfg ? cfg->vec_bytes : 0;
-  if (cfg && cfg->block != 0 && !((cfg->block == kBlock && variant != RD_VARIANT_BULK) ||
-                                   (cfg->block == 32 * (kBulkConsumerWarps + 1) && variant == RD_VARIANT_BULK))) {
-    set_error("block size not compiled for this variant");
+  if (cfg && cfg->block != 0 && !(cfg->block == kBlock && variant != RD_VARIANT_BULK)) {
+    set_error("block size not compiled for this variant (only the vector/paper variants' 256)");
     return RD_ERR_UNSUPPORTED;
   }
   if (variant < RD_VARIANT_AUTO || variant > RD_VARIANT_BULK || unroll < 0 || vec_bytes < 0 ||

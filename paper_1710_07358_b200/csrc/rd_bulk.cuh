@@ -144,11 +144,13 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   } else {
     // ---------------------------------------------------------------- consumers
     const int t = threadIdx.x;  // 0 .. CT-1
-    Acc acc[L];
+    using LO = LaneOps<OpT>;
+    typename LO::Lane acc[L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) acc[l] = OpT::identity();
+    for (int l = 0; l < L; ++l) acc[l] = LO::identity();
     int stage = 0;
     uint32_t phase = 0, nchunk_local = 0;
+    uint32_t cstage = 0;   // stage number within the current chunk
     const uint32_t ring_addr = smem_addr(ring);
     for (;;) {
       mbar_wait(&full[stage], phase);
@@ -157,8 +159,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
       const uint32_t bytes = st_bytes[stage];
       const uint32_t last = st_last[stage];
       const uint32_t base = ring_addr + stage * STAGE_BYTES;
-      // global element index of this stage's first element (indexed ops only)
-      const uint64_t e0 = OpT::kIndexed ? args.head + st_off[stage] / sizeof(T) : 0;
+      const uint32_t step0 = cstage * PER_THREAD;   // steps grow with the element index
       if (bytes == STAGE_BYTES) {
         uint4 v[PER_THREAD];
 #pragma unroll
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
         for (int k = 0; k < PER_THREAD; ++k) {
           Vec<16> w{{v[k].x, v[k].y, v[k].z, v[k].w}};
 #pragma unroll
-          for (int l = 0; l < L; ++l) acc[l] = fold_at<OpT>(acc[l], lane<T, 16>(w, l), e0 + (k * CT + t) * L + l);
+          for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, 16>(w, l), step0 + k);
         }
       } else {
 #pragma unroll
@@ -177,17 +178,24 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
             uint4 q = lds128(base + off);
             Vec<16> w{{q.x, q.y, q.z, q.w}};
 #pragma unroll
-            for (int l = 0; l < L; ++l) acc[l] = fold_at<OpT>(acc[l], lane<T, 16>(w, l), e0 + (k * CT + t) * L + l);
+            for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, 16>(w, l), step0 + k);
           }
         }
       }
       __syncwarp();
       if (ln == 0) mbar_arrive(&empty[stage]);
+      ++cstage;
       if (last) {
         // the chunk's partial: fixed tree over (thread, lane) -> independent of the schedule
-        Acc a = acc[0];
+        uint64_t coff = 0, clen = 0;
+        if constexpr (OpT::kIndexed) chunk_range(args, (uint32_t)c, body_bytes, &coff, &clen);
+        const uint64_t e_chunk = args.head + coff / sizeof(T);
+        Acc a = OpT::identity();
 #pragma unroll
-        for (int l = 1; l < L; ++l) a = OpT::combine(a, acc[l]);
+        for (int l = 0; l < L; ++l)
+          a = OpT::combine(a, LO::finish(acc[l], [&](uint32_t st) {
+                return e_chunk + ((uint64_t)(st / PER_THREAD) * (STAGE_BYTES / 16) + (st % PER_THREAD) * CT + t) * L + l;
+              }));
         a = OpT::warp_reduce(a);
         Acc* wp = wpart + (nchunk_local & 1) * CW;
         if (ln == 0) wp[warp] = a;
@@ -201,8 +209,9 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
           }
         }
         ++nchunk_local;
+        cstage = 0;
 #pragma unroll
-        for (int l = 0; l < L; ++l) acc[l] = OpT::identity();
+        for (int l = 0; l < L; ++l) acc[l] = LO::identity();
       }
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }

@@ -205,9 +205,10 @@ __global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
   static_assert(L >= 1, "vector narrower than the element");
   __shared__ Acc smem[32];
 
-  Acc acc[L];
+  using LO = LaneOps<OpT>;
+  typename LO::Lane acc[L];
 #pragma unroll
-  for (int l = 0; l < L; ++l) acc[l] = OpT::identity();
+  for (int l = 0; l < L; ++l) acc[l] = LO::identity();
 
   const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * B;
@@ -215,33 +216,33 @@ __global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
   pdl_wait();
   const uint64_t nvec = args.nvec;
   uint64_t i = tid;
+  uint32_t step = 0;   // vector slot tid + step*stride (indexed ops only)
   if constexpr (U > 1) {
-    for (; i + (uint64_t)(U - 1) * stride < nvec; i += (uint64_t)U * stride) {
+    for (; i + (uint64_t)(U - 1) * stride < nvec; i += (uint64_t)U * stride, step += U) {
       Vec<VB> v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int l = 0; l < L; ++l)
-          acc[l] = fold_at<OpT>(acc[l], lane<T, VB>(v[u], l), args.head + (i + (uint64_t)u * stride) * L + l);
+        for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, VB>(v[u], l), step + u);
     }
   }
-  for (; i < nvec; i += stride) {
+  for (; i < nvec; i += stride, ++step) {
     Vec<VB> v = ldg_stream<VB>(body + i * VB);
 #pragma unroll
-    for (int l = 0; l < L; ++l) acc[l] = fold_at<OpT>(acc[l], lane<T, VB>(v, l), args.head + i * L + l);
+    for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, VB>(v, l), step);
   }
-  // a2: head and tail stragglers
-  if (tid < args.head) acc[0] = fold_at<OpT>(acc[0], ldg_scalar<T>(args.x + tid * sizeof(T)), tid);
-  if (tid < args.tail)
-    acc[L - 1] = fold_at<OpT>(acc[L - 1], ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T)),
-                              args.tail_start + tid);
   pdl_trigger();
-  // a3
-  Acc a = acc[0];
+  // a3: lanes -> one accumulator (indexed ops: element index = head + (tid + step*stride)*L + l)
+  Acc a = OpT::identity();
 #pragma unroll
-  for (int l = 1; l < L; ++l) a = OpT::combine(a, acc[l]);
+  for (int l = 0; l < L; ++l)
+    a = OpT::combine(a, LO::finish(acc[l], [&](uint32_t st) { return args.head + (tid + (uint64_t)st * stride) * L + l; }));
+  // a2: head and tail stragglers
+  if (tid < args.head) a = fold_at<OpT>(a, ldg_scalar<T>(args.x + tid * sizeof(T)), tid);
+  if (tid < args.tail)
+    a = fold_at<OpT>(a, ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T)), args.tail_start + tid);
   // a4, a5
   a = block_reduce<OpT, B>(a, smem);
   __syncthreads();  // smem is reused by the grid combine

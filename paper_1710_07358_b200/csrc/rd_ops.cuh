@@ -332,6 +332,7 @@ struct Float64SumComp {
 template <typename U, rd_dtype DT, rd_op OP>
 struct ArgOp {
   using T = U;
+  static constexpr bool kMin = (OP == RD_ARGMIN);
   struct Acc { U key; uint64_t idx; };
   static constexpr bool kFloat = (DT == RD_FLOAT32 || DT == RD_FLOAT64);
   static constexpr bool kIndexed = true;
@@ -344,9 +345,14 @@ struct ArgOp {
     if constexpr (DT == RD_UINT32) return b;
     else if constexpr (!kFloat) return b ^ kSign;
     else {
-      if ((b & kAbs) > kInf) return OP == RD_ARGMIN ? (U)0 : (U)~(U)0;   // NaN wins
-      const U skey = b ^ ((U)((typename std::make_signed<U>::type)b >> (kBits - 1)) & kAbs);
-      return skey ^ kSign;
+      // unsigned total-order key in two ops: negative -> ~b, positive -> b ^ sign
+      const U sgn = (U)((typename std::make_signed<U>::type)b >> (kBits - 1));
+      const U k = b ^ (sgn | kSign);
+      // any NaN wins (maps to the winning end); one unordered float compare
+      bool nan;
+      if constexpr (sizeof(U) == 4) { const float f = __uint_as_float((uint32_t)b); nan = (f != f); }
+      else { const double f = __longlong_as_double((long long)b); nan = (f != f); }
+      return nan ? (OP == RD_ARGMIN ? (U)0 : (U)~(U)0) : k;
     }
   }
   __device__ __forceinline__ static U bits_of(U k) {   // inverse of key_of (non-NaN)
@@ -412,6 +418,44 @@ __device__ __forceinline__ typename OpT::Acc shifted(typename OpT::Acc a, uint64
   }
   return a;
 }
+
+#define OP_IS_MIN(OpT) (OpT::kMin)
+
+// ---------------------------------------------------------- lane accumulators
+// What the hot loops keep per (thread, vector lane). For plain ops it is the
+// op's accumulator. For indexed ops (argmin / argmax) it is the best order key
+// and the STEP at which it was seen: along one lane the element index grows
+// with the step, so a strict comparison keeps the earliest of equal keys and
+// the 64-bit global index is only formed once, in finish().
+template <class OpT, bool IDX = OpT::kIndexed>
+struct LaneOps {
+  using Lane = typename OpT::Acc;
+  __device__ __forceinline__ static Lane identity() { return OpT::identity(); }
+  __device__ __forceinline__ static Lane fold(Lane a, typename OpT::T x, uint32_t) { return OpT::fold(a, x); }
+  template <class F>
+  __device__ __forceinline__ static typename OpT::Acc finish(Lane a, F) { return a; }
+};
+
+template <class OpT>
+struct LaneOps<OpT, true> {
+  using T = typename OpT::T;
+  struct Lane { T key; uint32_t step; };
+  static constexpr uint32_t kEmpty = 0xffffffffu;
+  __device__ __forceinline__ static Lane identity() { return Lane{OpT::identity().key, kEmpty}; }
+  __device__ __forceinline__ static Lane fold(Lane a, T x, uint32_t step) {
+    const T k = OpT::key_of(x);
+    bool better = OP_IS_MIN(OpT) ? (k < a.key) : (k > a.key);
+    // float keys never reach the identity key; integer keys can, so an empty
+    // lane must take its first element unconditionally
+    if constexpr (!OpT::kFloat) better = better || (a.step == kEmpty);
+    return better ? Lane{k, step} : a;
+  }
+  template <class F>
+  __device__ __forceinline__ static typename OpT::Acc finish(Lane a, F index_of) {
+    if (a.step == kEmpty) return OpT::identity();
+    return typename OpT::Acc{a.key, index_of(a.step)};
+  }
+};
 
 // ---------------------------------------------------------------- type map
 template <rd_dtype DT, rd_op OP> struct OpFor;

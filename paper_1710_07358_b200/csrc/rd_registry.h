@@ -28,15 +28,19 @@ bool lookup_float(int dtype, int op, int variant, int unroll, int vec_bytes, Ker
 bool lookup_ablation(int dtype, int op, int variant, int unroll, int vec_bytes, KernelRef* r);
 CombineFn lookup_combine(int dtype, int op);
 
-// bulk variant: CW consumer warps + 1 producer warp per CTA
+// bulk variant: CW consumer warps + 1 producer warp per CTA. 8 consumer warps
+// keep up with HBM for the cheap combiners; the ALU-heavier float argmin /
+// argmax folds get 16 (more warps to hide the dependent integer chains).
 constexpr int kBulkConsumerWarps = 8;
+template <class OpT>
+struct BulkWarps { static constexpr int value = (OpT::kIndexed && OpT::kFloat) ? 16 : kBulkConsumerWarps; };
 
 template <class OpT, int STAGES, int STAGE_BYTES>
 inline bool bulk_entry(int stages, int stage_bytes, KernelRef* r) {
   if (stages != STAGES || stage_bytes != STAGE_BYTES) return false;
-  *r = KernelRef{rd_bulk_kernel<OpT, STAGES, STAGE_BYTES, kBulkConsumerWarps>, 32 * (kBulkConsumerWarps + 1),
-                 STAGES, STAGE_BYTES, RD_VARIANT_BULK,
-                 BulkSmem<STAGES, STAGE_BYTES, kBulkConsumerWarps>::kBytes};
+  constexpr int CW = BulkWarps<OpT>::value;
+  *r = KernelRef{rd_bulk_kernel<OpT, STAGES, STAGE_BYTES, CW>, 32 * (CW + 1), STAGES, STAGE_BYTES,
+                 RD_VARIANT_BULK, BulkSmem<STAGES, STAGE_BYTES, CW>::kBytes};
   return true;
 }
 

@@ -149,7 +149,8 @@ def do_ops(args):
         n = 1 << log2n
         for dtype, op in pairs:
             x = make(n, dtype, inputs.default_workload(dtype, op))
-            o = torch.empty((), dtype=x.dtype, device="cuda")
+            o = torch.empty(2, dtype=torch.int64, device="cuda") if op in rd.ARG_OPS else \
+                torch.empty((), dtype=x.dtype, device="cuda")
             _, info = rd.reduce_ex(x, op, out=o)
             r = time_launch(lambda: rd.reduce(x, op, out=o), n * SIZE[dtype])
             r.update({"dtype": dtype, "op": op, "n": n, "grid": info["grid"], "regs": info["regs_per_thread"],
