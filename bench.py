@@ -175,8 +175,13 @@ def run_b200(args):
             raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}: launch with torchrun")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    use_comm = ws > 1 or args.force_comm
+    if use_comm:
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     dt, op = args.dtype, args.op
     s = NP_BYTES[dt]
@@ -185,7 +190,7 @@ def run_b200(args):
     x = torch.empty(n, dtype=getattr(torch, dt), device=dev)
     inputs.fill_device(x, wl, seed=1, offset=rank * n, n_total=n * ws)
     out = torch.empty((), dtype=x.dtype, device=dev)
-    comm = rd.Comm.from_process_group() if ws > 1 else None
+    comm = rd.Comm.from_process_group() if use_comm else None
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -195,7 +200,7 @@ def run_b200(args):
             comm.reduce(x, op, out=out)
 
     def barrier():
-        if ws > 1:
+        if use_comm:
             import torch.distributed as dist
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -228,7 +233,7 @@ def run_b200(args):
     clocks = sampler.stop()
     total_ms = t0.elapsed_time(t1)
     local_ms = total_ms
-    if ws > 1:
+    if use_comm:
         import torch.distributed as dist
         tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -342,7 +347,7 @@ def run_b200(args):
             "context": {"torch_sum_gbs": tctx, "result": res},
         }
         print(json.dumps(line), flush=True)
-    if ws > 1:
+    if use_comm:
         import torch.distributed as dist
         dist.barrier()
         comm.destroy()
@@ -361,6 +366,8 @@ def main():
     p.add_argument("--log2n", type=int, default=28)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--force-comm", action="store_true",
+                   help="use the reduce_multi (NCCL) step even at one rank (tests the N>1 path on one GPU)")
     p.add_argument("--profile", action="store_true",
                    help="for ncu: no clock soak, e2e, cpu baseline or context rows (not a bench value)")
     args = p.parse_args()
