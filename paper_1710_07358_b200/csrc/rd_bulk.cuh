@@ -182,8 +182,14 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
           }
         }
       }
+      // release the stage: this warp's generic-proxy reads of the ring (and of
+      // the stage metadata) are ordered before the producer's next async-proxy
+      // (cp.async.bulk) write into it by the proxy fence + mbarrier release
       __syncwarp();
-      if (ln == 0) mbar_arrive(&empty[stage]);
+      if (ln == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&empty[stage]);
+      }
       ++cstage;
       if (last) {
         // the chunk's partial: fixed tree over (thread, lane) -> independent of the schedule
