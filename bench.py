@@ -190,7 +190,10 @@ def run_b200(args):
     x = torch.empty(n, dtype=getattr(torch, dt), device=dev)
     inputs.fill_device(x, wl, seed=1, offset=rank * n, n_total=n * ws)
     out = torch.empty((), dtype=x.dtype, device=dev)
-    comm = rd.Comm.from_process_group() if use_comm else None
+    if use_comm and args.fused:
+        comm = rd.FusedComm.from_process_group()     # exchange fused into the reduce kernel (f1)
+    else:
+        comm = rd.Comm.from_process_group() if use_comm else None
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -332,7 +335,9 @@ def run_b200(args):
             "config": {"workload": f"{dt} {op}, n=2^{args.log2n} per GPU ({wl}, seed 1), BASELINE configs[1]",
                        "n_per_gpu": n, "n_total": n * ws, "op": op,
                        "l2": "input (%.2f GB/GPU) > 126 MB L2: no flush" % (n * s / 1e9),
-                       "parallelism": f"shard{ws}" if ws > 1 else "single"},
+                       "parallelism": f"shard{ws}" if ws > 1 else "single",
+                       "exchange": ("fused in-kernel (reduce_fused)" if args.fused else "NCCL all-gather (reduce_multi)")
+                       if use_comm else None},
             "pct_hbm_peak": round(100 * value / (peak * ws), 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
@@ -342,7 +347,7 @@ def run_b200(args):
                          "algorithmic_bytes_per_launch": n * s},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * (1 if comm is None else 2),
+            "gpu_launches": K * (1 if (comm is None or args.fused) else 2),
             "clocks": clocks,
             "context": {"torch_sum_gbs": tctx, "result": res},
         }
@@ -366,6 +371,8 @@ def main():
     p.add_argument("--log2n", type=int, default=28)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--fused", action="store_true",
+                   help="N>1: exchange partials inside the reduce kernel over NVLink (reduce_fused) instead of NCCL")
     p.add_argument("--force-comm", action="store_true",
                    help="use the reduce_multi (NCCL) step even at one rank (tests the N>1 path on one GPU)")
     p.add_argument("--profile", action="store_true",

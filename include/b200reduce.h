@@ -91,7 +91,8 @@ typedef enum {
   RD_ERR_MISALIGNED = 3,   /* base pointer not aligned to sizeof(dtype)                */
   RD_ERR_CUDA = 4,         /* CUDA launch / allocation / copy failure (rd_last_error)  */
   RD_ERR_NCCL = 5,         /* NCCL failure (rd_last_error)                             */
-  RD_ERR_MISMATCH = 6      /* ranks or records disagree on dtype/op                    */
+  RD_ERR_MISMATCH = 6,     /* ranks or records disagree on dtype/op                    */
+  RD_ERR_TIMEOUT = 7       /* fused exchange: a peer's record never arrived (~seconds) */
 } rd_status;
 
 /* A CUDA stream handle; identical to cudaStream_t / CUstream. */
@@ -179,6 +180,39 @@ rd_status rd_comm_check(rd_comm_t comm, rd_stream_t stream);
 /* Canonical contiguous split: rank r gets [begin, begin+count) with
  * count = n/W + (r < n%W). Pure host function. */
 rd_status rd_shard_range(uint64_t n, int nranks, int rank, uint64_t* begin, uint64_t* count);
+
+/* ------------------------------------------- fused multi-GPU
+ * reduce_fused -- the sharded reduction with the exchange step INSIDE the
+ * reduce kernel: the last CTA of rank r stores its rd_record into slot r of
+ * every rank's mailbox over NVLink (peer stores to CUDA-IPC-mapped device
+ * memory), publishes it with a system-scope release, waits for the W records
+ * of this call in its own mailbox and folds them in rank order. One kernel
+ * launch per rank; no NCCL call, no host synchronisation. Same results and
+ * contract as reduce_multi (bitwise-identical on all ranks).
+ *
+ * Setup (collective, every rank in the same order):
+ *   rd_fused_create(&f, nranks, rank, device, handle)   allocates this rank's
+ *       mailbox and writes its 64-byte IPC handle to host `handle`;
+ *   exchange the nranks handles (e.g. an all-gather over the process group);
+ *   rd_fused_connect(f, handles)                         opens the peers'.
+ * Single-process use (several virtual ranks, one or more devices):
+ *   rd_fused_mailbox(f, &ptr) and rd_fused_connect_local(f, ptrs) with the
+ *   nranks mailbox device pointers instead of IPC handles.
+ * Every rank must call reduce_fused the same number of times in the same
+ * order (epochs are counted per communicator); nranks <= 32. A peer that
+ * never arrives makes the kernel give up after ~4 s with RD_ERR_TIMEOUT
+ * (reported by rd_fused_check) instead of hanging. */
+typedef struct rd_fused* rd_fused_t;
+rd_status rd_fused_create(rd_fused_t* f, int nranks, int rank, int device, void* ipc_handle_out);
+rd_status rd_fused_connect(rd_fused_t f, const void* ipc_handles);
+rd_status rd_fused_mailbox(rd_fused_t f, void** mailbox);
+rd_status rd_fused_connect_local(rd_fused_t f, void* const* mailboxes);
+rd_status reduce_fused(const void* x_local, size_t n_local, rd_dtype dtype, rd_op op, void* out,
+                       rd_stream_t stream, rd_fused_t f);
+/* Synchronises `stream`; returns the first RD_ERR_MISMATCH / RD_ERR_TIMEOUT
+ * seen by reduce_fused on this communicator since the last check, and clears it. */
+rd_status rd_fused_check(rd_fused_t f, rd_stream_t stream);
+rd_status rd_fused_destroy(rd_fused_t f);
 
 /* ---------------------------------------------------------------- helpers */
 /* Host copy of the empty result (table above) into host_out (one element;

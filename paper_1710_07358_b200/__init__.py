@@ -22,7 +22,7 @@ from . import _lib
 from ._lib import ReduceError, check, lib
 
 __all__ = ["reduce", "reduce_partial", "combine_records", "reduce_host", "reduce_ex",
-           "reduce_multi", "Comm", "shard_range", "identity", "release_workspaces",
+           "reduce_multi", "Comm", "FusedComm", "shard_range", "identity", "release_workspaces",
            "ReduceError", "OPS", "RECORD_BYTES"]
 
 OPS = {"sum": _lib.RD_SUM, "prod": _lib.RD_PROD, "min": _lib.RD_MIN, "max": _lib.RD_MAX,
@@ -268,3 +268,66 @@ def reduce_multi(x_local, op: str, comm: Comm, out=None, stream=None):
                              _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
                              comm.handle), "reduce_multi")
     return _result(out, x_local.dtype, op)
+
+
+class FusedComm:
+    """Multi-GPU reduction with the exchange fused into the reduce kernel
+    (include/b200reduce.h reduce_fused): one launch per rank, peer
+    stores over NVLink into CUDA-IPC-mapped mailboxes, rank-order fold."""
+
+    def __init__(self, handle: int, nranks: int, rank: int, device: int):
+        self.handle, self.nranks, self.rank, self.device = handle, nranks, rank, device
+
+    @classmethod
+    def _create(cls, nranks: int, rank: int, device: int, want_ipc: bool):
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(64) if want_ipc else None
+        check(lib().rd_fused_create(ctypes.byref(h), nranks, rank, device, buf), "rd_fused_create")
+        return cls(h.value, nranks, rank, device), (buf.raw if want_ipc else None)
+
+    @classmethod
+    def from_process_group(cls, group=None, device: int | None = None) -> "FusedComm":
+        """One process per GPU: exchange the mailboxes' IPC handles over the group."""
+        torch = _torch()
+        import torch.distributed as dist
+        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        dev = torch.cuda.current_device() if device is None else device
+        comm, mine = cls._create(nranks, rank, dev, True)
+        handles = [None] * nranks
+        dist.all_gather_object(handles, mine, group=group)
+        blob = b"".join(handles)
+        check(lib().rd_fused_connect(comm.handle, blob), "rd_fused_connect")
+        return comm
+
+    @classmethod
+    def local(cls, nranks: int, device: int = 0) -> list:
+        """nranks virtual ranks in this process (tests, or several devices driven
+        by one process): mailboxes are connected by device pointer."""
+        comms = [cls._create(nranks, r, device, False)[0] for r in range(nranks)]
+        ptrs = (ctypes.c_void_p * nranks)()
+        for r, c in enumerate(comms):
+            p = ctypes.c_void_p()
+            check(lib().rd_fused_mailbox(c.handle, ctypes.byref(p)), "rd_fused_mailbox")
+            ptrs[r] = p
+        for c in comms:
+            check(lib().rd_fused_connect_local(c.handle, ptrs), "rd_fused_connect_local")
+        return comms
+
+    def reduce(self, x_local, op: str, out=None, stream=None):
+        _check_input(x_local)
+        out = _new_out(x_local.dtype, x_local.device, op) if out is None else _check_out(out, x_local.dtype, op)
+        check(lib().reduce_fused(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
+                                 _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
+                                 self.handle), "reduce_fused")
+        return _result(out, x_local.dtype, op)
+
+    def check(self, stream=None):
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        st = st.cuda_stream if hasattr(st, "cuda_stream") else st
+        check(lib().rd_fused_check(self.handle, st), "rd_fused_check")
+
+    def destroy(self):
+        if self.handle:
+            check(lib().rd_fused_destroy(self.handle), "rd_fused_destroy")
+            self.handle = None

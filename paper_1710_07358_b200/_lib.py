@@ -16,7 +16,7 @@ RD_SUM, RD_PROD, RD_MIN, RD_MAX, RD_AND, RD_OR, RD_XOR = range(7)
 RD_ARGMIN, RD_ARGMAX, RD_SUM_COMPENSATED = 7, 8, 9
 RD_OK = 0
 STATUS = {0: "RD_OK", 1: "RD_ERR_INVALID_ARG", 2: "RD_ERR_UNSUPPORTED", 3: "RD_ERR_MISALIGNED",
-          4: "RD_ERR_CUDA", 5: "RD_ERR_NCCL", 6: "RD_ERR_MISMATCH"}
+          4: "RD_ERR_CUDA", 5: "RD_ERR_NCCL", 6: "RD_ERR_MISMATCH", 7: "RD_ERR_TIMEOUT"}
 RD_VARIANT_AUTO, RD_VARIANT_VECTOR, RD_VARIANT_PAPER, RD_VARIANT_BULK = 0, 1, 2, 3
 
 
@@ -64,6 +64,13 @@ SIGNATURES = {
     "rd_last_error": (ctypes.c_char_p, []),
     "rd_reduce_ex": (_i, [_vp, _sz, _i, _i, _vp, _vp, ctypes.POINTER(rd_config),
                           ctypes.POINTER(rd_launch_info)]),
+    "rd_fused_create": (_i, [ctypes.POINTER(_vp), _i, _i, _i, _vp]),
+    "rd_fused_connect": (_i, [_vp, _vp]),
+    "rd_fused_mailbox": (_i, [_vp, ctypes.POINTER(_vp)]),
+    "rd_fused_connect_local": (_i, [_vp, ctypes.POINTER(_vp)]),
+    "reduce_fused": (_i, [_vp, _sz, _i, _i, _vp, _vp, _vp]),
+    "rd_fused_check": (_i, [_vp, _vp]),
+    "rd_fused_destroy": (_i, [_vp]),
 }
 
 _lib = None

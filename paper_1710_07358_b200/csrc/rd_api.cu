@@ -75,8 +75,9 @@ rd_status get_workspace(int dev, cudaStream_t stream, Workspace* out) {
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, sizeof(Slot) * kMaxSlots + 256);
   if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
-  e = cudaMemset(p, 0, sizeof(Slot) * kMaxSlots + 256);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  // zeroed in stream order (no device-wide synchronisation: kernels on other
+  // streams, e.g. the ranks of a fused exchange, may be running and waiting)
+  e = cudaMemsetAsync(p, 0, sizeof(Slot) * kMaxSlots + 256, stream);
   if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "workspace init"); }
   w.partials = (Slot*)p;
   w.ticket = (unsigned*)((char*)p + sizeof(Slot) * kMaxSlots);
@@ -130,18 +131,47 @@ bool lookup(int dtype, int op, int variant, int unroll, int vec_bytes, KernelRef
 
 }  // namespace
 
+// Load (and configure) every default kernel now. With CUDA lazy loading, the
+// first launch of a kernel loads it, and loading can wait for running kernels
+// to finish -- which deadlocks spinning producer/consumer kernels such as
+// the ranks of a fused exchange driven from one process. Called when a fused
+// communicator is connected.
+rd_status preload_default_kernels(int dev) {
+  for (int dt = RD_INT32; dt <= RD_FLOAT64; ++dt) {
+    for (int op = RD_SUM; op <= RD_SUM_COMPENSATED; ++op) {
+      if (check_dtype_op(dt, op) != RD_OK) continue;
+      for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK}) {
+        KernelRef k;
+        if (!lookup(dt, op, variant, 0, 0, &k)) continue;
+        int occ = 0, regs = 0;
+        rd_status st = occupancy(dev, k, &occ, &regs);
+        if (st != RD_OK) return st;
+      }
+      CombineFn c = lookup_combine(dt, op);
+      cudaFuncAttributes fa;
+      if (c) {
+        cudaError_t e = cudaFuncGetAttributes(&fa, c);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncGetAttributes(combine)");
+      }
+    }
+  }
+  set_error("");
+  return RD_OK;
+}
+
 // a0: validate, plan, launch.
 rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, void* out,
                         rd_record* rec, cudaStream_t stream, const rd_config* cfg,
-                        rd_launch_info* info) {
+                        rd_launch_info* info, const FusedArgs* fused) {
   rd_status st = check_dtype_op(dtype, op);
   if (st != RD_OK) return st;
   const int s = dtype_size(dtype);
   if (x == nullptr && n > 0) { set_error("x is NULL"); return RD_ERR_INVALID_ARG; }
-  if (mode == 0 && out == nullptr) { set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
+  if ((mode == 0 || mode == 2) && out == nullptr) { set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
+  if (mode == 2 && fused == nullptr) { set_error("fused args missing"); return RD_ERR_INVALID_ARG; }
   if (mode == 1 && rec == nullptr) { set_error("rec is NULL"); return RD_ERR_INVALID_ARG; }
   if ((uintptr_t)x % s != 0) { set_error("x is not aligned to sizeof(dtype)"); return RD_ERR_MISALIGNED; }
-  if (mode == 0 && (uintptr_t)out % (is_arg_op(op) ? 8 : s) != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
+  if (mode != 1 && (uintptr_t)out % (is_arg_op(op) ? 8 : s) != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
   if (mode == 1 && (uintptr_t)rec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
 
@@ -239,6 +269,14 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   a.ticket = ws.ticket;
   a.tag = record_tag(dtype, op);
   a.mode = mode;
+  if (fused) {
+    a.peers = fused->peers;
+    a.self = fused->self;
+    a.err = fused->err;
+    a.epoch = fused->epoch;
+    a.nranks = fused->nranks;
+    a.rank = fused->rank;
+  }
 
   // programmatic dependent launch: the grid may be scheduled while the previous
   // kernel on the stream drains; the kernels call griddepcontrol.wait before
@@ -384,6 +422,7 @@ const char* rd_status_string(rd_status s) {
     case RD_ERR_CUDA: return "RD_ERR_CUDA";
     case RD_ERR_NCCL: return "RD_ERR_NCCL";
     case RD_ERR_MISMATCH: return "RD_ERR_MISMATCH";
+    case RD_ERR_TIMEOUT: return "RD_ERR_TIMEOUT";
     default: return "RD_ERR_UNKNOWN";
   }
 }

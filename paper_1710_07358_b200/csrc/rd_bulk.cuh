@@ -241,10 +241,10 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
                      args.tail_start + threadIdx.x);
   b = block_reduce<OpT, B>(b, red);
   if (threadIdx.x == 0) {
-    finish<OpT>(b, args);
     *args.ticket = 0u;
     *args.work = 0u;
   }
+  if (threadIdx.x < 32) finish_warp0<OpT>(b, args);
 }
 
 }  // namespace rd

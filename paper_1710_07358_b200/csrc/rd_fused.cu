@@ -1,0 +1,150 @@
+// rd_fused.cu -- SURVEY f1: the multi-GPU exchange fused into the reduce
+// kernel (rd_kernels.cuh fused_exchange). Host side: mailbox allocation, CUDA
+// IPC handle export / import, epoch counting, error readback.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <vector>
+
+#include "b200reduce.h"
+#include "rd_internal.h"
+#include "rd_kernels.cuh"
+
+static_assert(sizeof(cudaIpcMemHandle_t) <= 64, "IPC handle fits the 64-byte slot");
+
+struct rd_fused {
+  int nranks = 0, rank = 0, device = 0;
+  rd::Mailbox* self = nullptr;          // this rank's mailbox (+ err word after it)
+  int* d_err = nullptr;
+  rd::Mailbox** d_peers = nullptr;      // device array of nranks pointers
+  std::vector<void*> opened;            // IPC-opened peer mappings to close
+  uint64_t epoch = 0;
+  bool connected = false;
+};
+
+namespace {
+rd_status upload_peers(rd_fused* f, const std::vector<rd::Mailbox*>& ptrs) {
+  cudaError_t e = cudaMemcpy(f->d_peers, ptrs.data(), sizeof(rd::Mailbox*) * f->nranks, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemcpy(peers)");
+  // no lazy kernel loading once ranks may be spinning (rd_api.cu)
+  rd_status st = rd::preload_default_kernels(f->device);
+  if (st != RD_OK) return st;
+  f->connected = true;
+  return RD_OK;
+}
+}  // namespace
+
+extern "C" {
+
+rd_status rd_fused_create(rd_fused_t* out, int nranks, int rank, int device, void* ipc_handle_out) {
+  if (!out || nranks < 1 || nranks > rd::kMaxRanks || rank < 0 || rank >= nranks || device < 0) {
+    rd::set_error("bad rd_fused_create arguments (nranks <= 32)");
+    return RD_ERR_INVALID_ARG;
+  }
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaSetDevice");
+  rd_fused* f = new rd_fused();
+  f->nranks = nranks;
+  f->rank = rank;
+  f->device = device;
+  void* p = nullptr;
+  const size_t bytes = sizeof(rd::Mailbox) + 256;
+  e = cudaMalloc(&p, bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&f->d_peers, sizeof(rd::Mailbox*) * rd::kMaxRanks);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cudaFree(p); delete f; return rd::cuda_fail(e, "mailbox allocation"); }
+  f->self = (rd::Mailbox*)p;
+  f->d_err = (int*)((char*)p + sizeof(rd::Mailbox));
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) { cudaFree(p); cudaFree(f->d_peers); delete f; return rd::cuda_fail(e, "cudaIpcGetMemHandle"); }
+    std::memset(ipc_handle_out, 0, 64);
+    std::memcpy(ipc_handle_out, &h, sizeof(h));
+  }
+  *out = f;
+  return RD_OK;
+}
+
+rd_status rd_fused_connect(rd_fused_t f, const void* ipc_handles) {
+  if (!f || !ipc_handles) { rd::set_error("bad rd_fused_connect arguments"); return RD_ERR_INVALID_ARG; }
+  cudaError_t e = cudaSetDevice(f->device);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaSetDevice");
+  std::vector<rd::Mailbox*> ptrs(f->nranks);
+  for (int p = 0; p < f->nranks; ++p) {
+    if (p == f->rank) { ptrs[p] = f->self; continue; }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, (const char*)ipc_handles + 64 * p, sizeof(h));
+    void* q = nullptr;
+    e = cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return rd::cuda_fail(e, "cudaIpcOpenMemHandle");
+    f->opened.push_back(q);
+    ptrs[p] = (rd::Mailbox*)q;
+  }
+  return upload_peers(f, ptrs);
+}
+
+rd_status rd_fused_mailbox(rd_fused_t f, void** mailbox) {
+  if (!f || !mailbox) { rd::set_error("bad rd_fused_mailbox arguments"); return RD_ERR_INVALID_ARG; }
+  *mailbox = f->self;
+  return RD_OK;
+}
+
+rd_status rd_fused_connect_local(rd_fused_t f, void* const* mailboxes) {
+  if (!f || !mailboxes) { rd::set_error("bad rd_fused_connect_local arguments"); return RD_ERR_INVALID_ARG; }
+  std::vector<rd::Mailbox*> ptrs(f->nranks);
+  for (int p = 0; p < f->nranks; ++p) {
+    if (!mailboxes[p]) { rd::set_error("NULL mailbox"); return RD_ERR_INVALID_ARG; }
+    ptrs[p] = (rd::Mailbox*)mailboxes[p];
+  }
+  if (ptrs[f->rank] != f->self) { rd::set_error("mailboxes[rank] is not this rank's mailbox"); return RD_ERR_INVALID_ARG; }
+  cudaError_t e = cudaSetDevice(f->device);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaSetDevice");
+  return upload_peers(f, ptrs);
+}
+
+rd_status reduce_fused(const void* x_local, size_t n_local, rd_dtype dtype, rd_op op, void* out,
+                       rd_stream_t stream, rd_fused_t f) {
+  if (!f) { rd::set_error("fused communicator is NULL"); return RD_ERR_INVALID_ARG; }
+  if (!f->connected) { rd::set_error("fused communicator not connected"); return RD_ERR_INVALID_ARG; }
+  rd::FusedArgs fa;
+  fa.peers = f->d_peers;
+  fa.self = f->self;
+  fa.err = f->d_err;
+  fa.epoch = f->epoch + 1;
+  fa.nranks = f->nranks;
+  fa.rank = f->rank;
+  rd_status st = rd::launch_reduce(x_local, n_local, dtype, op, 2, out, nullptr, (cudaStream_t)stream,
+                                   nullptr, nullptr, &fa);
+  if (st == RD_OK) f->epoch = fa.epoch;   // count only launched calls
+  return st;
+}
+
+rd_status rd_fused_check(rd_fused_t f, rd_stream_t stream) {
+  if (!f) { rd::set_error("fused communicator is NULL"); return RD_ERR_INVALID_ARG; }
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaStreamSynchronize");
+  int h = 0;
+  e = cudaMemcpy(&h, f->d_err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemcpy");
+  if (h) {
+    cudaMemset(f->d_err, 0, sizeof(int));
+    rd::set_error(h == RD_ERR_TIMEOUT ? "a peer's record never arrived" : "ranks disagree on dtype/op");
+    return (rd_status)h;
+  }
+  return RD_OK;
+}
+
+rd_status rd_fused_destroy(rd_fused_t f) {
+  if (!f) { rd::set_error("fused communicator is NULL"); return RD_ERR_INVALID_ARG; }
+  cudaSetDevice(f->device);
+  cudaDeviceSynchronize();
+  for (void* q : f->opened) cudaIpcCloseMemHandle(q);
+  cudaFree(f->d_peers);
+  cudaFree(f->self);
+  delete f;
+  return RD_OK;
+}
+
+}  // extern "C"

@@ -19,15 +19,29 @@ int dtype_size(int dtype);
 bool is_arg_op(int op);
 int out_size(int dtype, int op);   // bytes of one result: element, or rd_arg_result
 
+struct Mailbox;
+// mode 2 (fused exchange) parameters
+struct FusedArgs {
+  Mailbox* const* peers;   // device array of nranks mailbox pointers
+  Mailbox* self;
+  int* err;
+  uint64_t epoch;
+  int nranks, rank;
+};
+
 // Plan + launch one reduction of x[0..n) (a0-a7). mode 0 writes one element
-// to `out`, mode 1 writes one rd_record to `rec`.
+// to `out`, mode 1 writes one rd_record to `rec`, mode 2 exchanges records
+// through the mailboxes of `fused` and writes the folded result to `out`.
 rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, void* out,
                         rd_record* rec, cudaStream_t stream, const rd_config* cfg,
-                        rd_launch_info* info);
+                        rd_launch_info* info, const FusedArgs* fused = nullptr);
 
 // Launch the record-combine kernel (N4).
 rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, void* out,
                          rd_record* rec_out, int* d_status, cudaStream_t stream);
+
+// load every default kernel up front (see rd_api.cu)
+rd_status preload_default_kernels(int dev);
 
 // per-(device) cleanup hooks of the other translation units
 void release_host_pipelines();

@@ -27,6 +27,17 @@
 
 namespace rd {
 
+// Fused-exchange mailbox: one per rank, in device memory that every
+// rank can address (CUDA IPC over NVLink, or the same device in tests).
+// Slots are double-buffered by epoch parity: a rank can be at most one
+// reduction ahead of a peer (it cannot finish epoch e+1 before that peer has
+// sent its e+1 record, which the peer does only after folding epoch e).
+constexpr int kMaxRanks = 32;
+struct Mailbox {
+  rd_record rec[2][kMaxRanks];
+  unsigned long long flag[2][kMaxRanks];   // epoch of the record in rec[par][sender]
+};
+
 struct KArgs {
   const unsigned char* x;   // element 0
   uint64_t n;               // elements
@@ -46,6 +57,12 @@ struct KArgs {
   uint32_t nchunks;         // chunks in the body
   uint32_t nhead_chunks;    // chunks of size C0; the rest have size C1
   unsigned* work;           // dynamic chunk counter, zero between launches
+  // mode 2 (fused multi-GPU exchange) only
+  Mailbox* const* peers;    // device array: peers[p] = rank p's mailbox
+  Mailbox* self;            // this rank's mailbox
+  int* err;                 // sticky status (RD_ERR_MISMATCH / RD_ERR_TIMEOUT)
+  uint64_t epoch;           // 1, 2, 3, ... per call on this communicator
+  int nranks, rank;
 };
 
 // Programmatic dependent launch: a kernel launched right behind another may be
@@ -148,6 +165,78 @@ __device__ __forceinline__ void finish(const typename OpT::Acc& a, const KArgs& 
   }
 }
 
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// a8 fused into the kernel: warp 0 of the last CTA pushes this
+// rank's record into slot [epoch&1][rank] of every peer's mailbox (peer
+// stores over NVLink), publishes it with a system-scope release of the
+// epoch, waits for the W records of this epoch in its own mailbox, and folds
+// them in RANK ORDER -- every rank computes the identical result, with no
+// host call and no second kernel. A bounded wait reports RD_ERR_TIMEOUT.
+template <class OpT>
+__device__ __noinline__ void fused_exchange(typename OpT::Acc a, const KArgs& args) {
+  const int ln = threadIdx.x & 31;
+  Slot s = OpT::pack(a);                               // valid in lane 0
+  s.a = __shfl_sync(0xffffffffu, s.a, 0);
+  s.b = __shfl_sync(0xffffffffu, s.b, 0);
+  const int par = (int)(args.epoch & 1);
+  const int W = args.nranks;
+  for (int p = ln; p < W; p += 32) {
+    Mailbox* dst = args.peers[p];
+    volatile unsigned long long* r = reinterpret_cast<volatile unsigned long long*>(&dst->rec[par][args.rank]);
+    r[0] = (unsigned long long)args.tag;               // tag (low 32) | status 0 (high 32)
+    r[1] = args.n;
+    r[2] = s.a;
+    r[3] = s.b;
+    __threadfence_system();
+    st_release_sys(&dst->flag[par][args.rank], args.epoch);
+  }
+  bool timeout = false;
+  for (int q = ln; q < W; q += 32) {
+    uint32_t spins = 0;
+    while (ld_acquire_sys(&args.self->flag[par][q]) != args.epoch) {
+      __nanosleep(64);
+      if (++spins > (1u << 26)) { timeout = true; break; }
+    }
+  }
+  timeout = __any_sync(0xffffffffu, timeout);
+  if (ln == 0) {
+    using Acc = typename OpT::Acc;
+    Acc acc = OpT::identity();
+    uint64_t nn = 0;
+    bool bad = false;
+    for (int q = 0; q < W && !timeout; ++q) {
+      (void)ld_acquire_sys(&args.self->flag[par][q]);  // acquire in this thread too
+      const volatile unsigned long long* r =
+          reinterpret_cast<const volatile unsigned long long*>(&args.self->rec[par][q]);
+      const uint32_t tag = (uint32_t)r[0];
+      const uint64_t n = r[1];
+      const Slot sl{r[2], r[3]};
+      if (tag != args.tag) { bad = true; continue; }
+      acc = OpT::combine(acc, shifted<OpT>(OpT::unpack(sl), nn));
+      nn += n;
+    }
+    if (timeout) atomicExch(args.err, (int)RD_ERR_TIMEOUT);
+    else if (bad) atomicExch(args.err, (int)RD_ERR_MISMATCH);
+    if (timeout || bad || nn == 0) OpT::store_empty(args.out);
+    else OpT::store(acc, args.out);
+  }
+}
+
+// the end of every reduce kernel: warp 0 of the finishing CTA, result in lane 0
+template <class OpT>
+__device__ __forceinline__ void finish_warp0(const typename OpT::Acc& a, const KArgs& args) {
+  if (args.mode == 2) fused_exchange<OpT>(a, args);
+  else if ((threadIdx.x & 31) == 0) finish<OpT>(a, args);
+}
+
 // Thread t folds slots t, t+B, t+2B, ... in increasing order (a fixed tree);
 // 8 independent loads in flight per thread.
 template <class OpT, int B>
@@ -174,7 +263,7 @@ __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& a
                                              typename OpT::Acc* smem) {
   using Acc = typename OpT::Acc;
   if (gridDim.x == 1) {
-    if (threadIdx.x == 0) finish<OpT>(a, args);
+    if (threadIdx.x < 32) finish_warp0<OpT>(a, args);
     return;
   }
   __shared__ unsigned s_last;
@@ -190,10 +279,8 @@ __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& a
   __threadfence();                                     // acquire the other partials
   Acc b = fold_slots<OpT, B>(args.partials, gridDim.x);
   b = block_reduce<OpT, B>(b, smem);
-  if (threadIdx.x == 0) {
-    finish<OpT>(b, args);
-    *args.ticket = 0u;                                 // reusable by the next launch
-  }
+  if (threadIdx.x == 0) *args.ticket = 0u;             // reusable by the next launch
+  if (threadIdx.x < 32) finish_warp0<OpT>(b, args);
 }
 
 // ---------------------------------------------------------------- a1-a7

@@ -38,7 +38,9 @@ def test_header_declares_the_boundary():
     for must in ["reduce", "reduce_partial", "reduce_multi", "rd_combine_records", "reduce_host",
                  "rd_get_unique_id", "rd_comm_init", "rd_comm_destroy", "rd_comm_check",
                  "rd_identity", "rd_release_workspaces", "rd_status_string", "rd_last_error",
-                 "rd_shard_range", "rd_reduce_ex"]:
+                 "rd_shard_range", "rd_reduce_ex", "reduce_fused", "rd_fused_create",
+                 "rd_fused_connect", "rd_fused_connect_local", "rd_fused_mailbox", "rd_fused_check",
+                 "rd_fused_destroy"]:
         assert must in names, must
 
 
@@ -104,6 +106,10 @@ def test_validation_before_any_device_work():
     assert L.rd_combine_records(None, 2, 0, 0, out, None, None, None) == 1
     assert L.rd_combine_records(None, -1, 0, 0, out, None, None, None) == 1
     assert L.reduce_multi(p, 4, 0, 0, out, None, None) == 1        # comm NULL
+    h = ctypes.c_void_p()
+    assert L.rd_fused_create(ctypes.byref(h), 33, 0, 0, None) == 1  # nranks > 32
+    assert L.rd_fused_create(ctypes.byref(h), 2, 2, 0, None) == 1   # rank out of range
+    assert L.reduce_fused(p, 4, 0, 0, out, None, None) == 1         # comm NULL
     cfg = _lib.rd_config(7, 0, 0, 0, 0)
     assert L.rd_reduce_ex(p, 4, 0, 0, out, None, ctypes.byref(cfg), None) == 1
     cfg = _lib.rd_config(1, 32, 3, 0, 0)                           # U=3 only for the ablation pairs

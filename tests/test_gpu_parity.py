@@ -531,3 +531,64 @@ def test_compensated_sum_full_size(rd, dtype, wl):
     ref = _parity.check(g, xh, "sum_compensated")
     assert g.tobytes() == np.array([ref.value]).astype(dtype).tobytes()
     assert variants == {g.tobytes()}
+
+
+# ------------------------------------------------------------------ f1: fused exchange
+@pytest.mark.parametrize("W", [1, 2, 3, 8])
+def test_fused_exchange_local_ranks(rd, W):
+    """reduce_fused with W virtual ranks on one GPU (mailboxes connected by
+    pointer, kernels on W concurrent streams): every rank returns the identical
+    result, equal to the oracle on the whole array, over several epochs (the
+    epoch-parity double buffering) and for plain, compensated and arg ops."""
+    comms = rd.FusedComm.local(W, torch.cuda.current_device())
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    try:
+        cases = [("float32", "sum", (1 << 20) + 7), ("float64", "argmax", 100003), ("int32", "xor", 5533214),
+                 ("float64", "prod", (1 << 16) + 1), ("float32", "sum_compensated", 1 << 25), ("int64", "min", 7)]
+        for rep in range(3):
+            for dtype, op, n in cases:
+                x = inputs.generate(n, dtype, inputs.default_workload(dtype, op), seed=rep + 1)
+                xd = to_dev(x, 1)
+                outs = []
+                for r in range(W):
+                    b, c = rd.shard_range(n, W, r)
+                    with torch.cuda.stream(streams[r]):
+                        outs.append(comms[r].reduce(xd[b:b + c], op))
+                torch.cuda.synchronize()
+                for r in range(W):
+                    comms[r].check(streams[r])
+                vals = [val(o) for o in outs]
+                for v in vals:
+                    assert repr(v) == repr(vals[0])
+                _parity.check(vals[0], x, op)
+    finally:
+        torch.cuda.synchronize()
+        for c in comms:
+            c.destroy()
+
+
+def test_fused_exchange_mismatch_and_timeout(rd):
+    comms = rd.FusedComm.local(2, torch.cuda.current_device())
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    try:
+        x = to_dev(inputs.generate(1000, "float32", "u01"))
+        with torch.cuda.stream(streams[0]):
+            comms[0].reduce(x, "sum")
+        with torch.cuda.stream(streams[1]):
+            comms[1].reduce(x, "max")
+        torch.cuda.synchronize()
+        for r in range(2):
+            with pytest.raises(rd.ReduceError) as e:
+                comms[r].check(streams[r])
+            assert e.value.status == 6
+        # rank 1 never calls: rank 0 gives up (RD_ERR_TIMEOUT) instead of hanging
+        with torch.cuda.stream(streams[0]):
+            comms[0].reduce(x, "sum")
+        torch.cuda.synchronize()
+        with pytest.raises(rd.ReduceError) as e:
+            comms[0].check(streams[0])
+        assert e.value.status == 7
+    finally:
+        torch.cuda.synchronize()
+        for c in comms:
+            c.destroy()
