@@ -199,7 +199,8 @@ rd_status rd_shard_range(uint64_t n, int nranks, int rank, uint64_t* begin, uint
  *   rd_fused_mailbox(f, &ptr) and rd_fused_connect_local(f, ptrs) with the
  *   nranks mailbox device pointers instead of IPC handles.
  * Every rank must call reduce_fused the same number of times in the same
- * order (epochs are counted per communicator); nranks <= 32. A peer that
+ * order (epochs are counted on the device, in each rank's mailbox, so the
+ * call can be captured in a CUDA graph and replayed); nranks <= 32. A peer that
  * never arrives makes the kernel give up after ~4 s with RD_ERR_TIMEOUT
  * (reported by rd_fused_check) instead of hanging. */
 typedef struct rd_fused* rd_fused_t;

@@ -273,7 +273,6 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     a.peers = fused->peers;
     a.self = fused->self;
     a.err = fused->err;
-    a.epoch = fused->epoch;
     a.nranks = fused->nranks;
     a.rank = fused->rank;
   }

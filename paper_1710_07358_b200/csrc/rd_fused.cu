@@ -18,7 +18,6 @@ struct rd_fused {
   int* d_err = nullptr;
   rd::Mailbox** d_peers = nullptr;      // device array of nranks pointers
   std::vector<void*> opened;            // IPC-opened peer mappings to close
-  uint64_t epoch = 0;
   bool connected = false;
 };
 
@@ -112,13 +111,10 @@ rd_status reduce_fused(const void* x_local, size_t n_local, rd_dtype dtype, rd_o
   fa.peers = f->d_peers;
   fa.self = f->self;
   fa.err = f->d_err;
-  fa.epoch = f->epoch + 1;
   fa.nranks = f->nranks;
   fa.rank = f->rank;
-  rd_status st = rd::launch_reduce(x_local, n_local, dtype, op, 2, out, nullptr, (cudaStream_t)stream,
-                                   nullptr, nullptr, &fa);
-  if (st == RD_OK) f->epoch = fa.epoch;   // count only launched calls
-  return st;
+  return rd::launch_reduce(x_local, n_local, dtype, op, 2, out, nullptr, (cudaStream_t)stream,
+                           nullptr, nullptr, &fa);
 }
 
 rd_status rd_fused_check(rd_fused_t f, rd_stream_t stream) {

@@ -25,7 +25,6 @@ struct FusedArgs {
   Mailbox* const* peers;   // device array of nranks mailbox pointers
   Mailbox* self;
   int* err;
-  uint64_t epoch;
   int nranks, rank;
 };
 

@@ -36,6 +36,8 @@ constexpr int kMaxRanks = 32;
 struct Mailbox {
   rd_record rec[2][kMaxRanks];
   unsigned long long flag[2][kMaxRanks];   // epoch of the record in rec[par][sender]
+  unsigned long long epoch;                // calls completed by this rank (device-side:
+                                           // the exchange is CUDA-graph capturable)
 };
 
 struct KArgs {
@@ -61,7 +63,6 @@ struct KArgs {
   Mailbox* const* peers;    // device array: peers[p] = rank p's mailbox
   Mailbox* self;            // this rank's mailbox
   int* err;                 // sticky status (RD_ERR_MISMATCH / RD_ERR_TIMEOUT)
-  uint64_t epoch;           // 1, 2, 3, ... per call on this communicator
   int nranks, rank;
 };
 
@@ -186,7 +187,10 @@ __device__ __noinline__ void fused_exchange(typename OpT::Acc a, const KArgs& ar
   Slot s = OpT::pack(a);                               // valid in lane 0
   s.a = __shfl_sync(0xffffffffu, s.a, 0);
   s.b = __shfl_sync(0xffffffffu, s.b, 0);
-  const int par = (int)(args.epoch & 1);
+  // this call's epoch: calls on one rank are stream-ordered, so the counter in
+  // its own mailbox is read and bumped without races
+  const unsigned long long epoch = *(volatile unsigned long long*)&args.self->epoch + 1;
+  const int par = (int)(epoch & 1);
   const int W = args.nranks;
   for (int p = ln; p < W; p += 32) {
     Mailbox* dst = args.peers[p];
@@ -195,15 +199,15 @@ __device__ __noinline__ void fused_exchange(typename OpT::Acc a, const KArgs& ar
     r[1] = args.n;
     r[2] = s.a;
     r[3] = s.b;
-    __threadfence_system();
-    st_release_sys(&dst->flag[par][args.rank], args.epoch);
+    // the release orders the record stores above before the flag (no full fence)
+    st_release_sys(&dst->flag[par][args.rank], epoch);
   }
   bool timeout = false;
   for (int q = ln; q < W; q += 32) {
     uint32_t spins = 0;
-    while (ld_acquire_sys(&args.self->flag[par][q]) != args.epoch) {
-      __nanosleep(64);
-      if (++spins > (1u << 26)) { timeout = true; break; }
+    while (ld_acquire_sys(&args.self->flag[par][q]) != epoch) {
+      if (++spins > 4096) __nanosleep(128);           // tight spin first, then back off
+      if (spins > (1u << 25)) { timeout = true; break; }
     }
   }
   timeout = __any_sync(0xffffffffu, timeout);
@@ -227,6 +231,7 @@ __device__ __noinline__ void fused_exchange(typename OpT::Acc a, const KArgs& ar
     else if (bad) atomicExch(args.err, (int)RD_ERR_MISMATCH);
     if (timeout || bad || nn == 0) OpT::store_empty(args.out);
     else OpT::store(acc, args.out);
+    *(volatile unsigned long long*)&args.self->epoch = epoch;
   }
 }
 

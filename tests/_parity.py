@@ -27,7 +27,7 @@ def to_bits(v, dtype):
 def check(got, x: np.ndarray, op: str, ref=None, factor: float = 4.0):
     """Assert parity of `got` (numpy scalar / python number; (value, index) for
     argmin / argmax) with the oracle on x."""
-    dtype = x.dtype.name
+    dtype = x.dtype.name          # with ref given, x only supplies the dtype
     r = ref if ref is not None else oracle.reduce(x, op)
     if op in ("argmin", "argmax"):
         gv, gi = got
@@ -44,7 +44,7 @@ def check(got, x: np.ndarray, op: str, ref=None, factor: float = 4.0):
             assert math.isnan(float(g)), f"{op}: want NaN, got {g}"
             return r
         assert to_bits(g, dtype) == to_bits(r.value, dtype), \
-            f"{dtype} {op} n={x.size}: got {g!r} want {r.value!r}"
+            f"{dtype} {op} n={r.count}: got {g!r} want {r.value!r}"
         return r
     want = float(r.value)
     gv = float(g)
@@ -64,7 +64,7 @@ def check(got, x: np.ndarray, op: str, ref=None, factor: float = 4.0):
     else:
         tol = factor * EPS[dtype] * abs(r.exact)
     err = abs(gv - r.exact)
-    assert err <= tol, f"{dtype} {op} n={x.size}: |{gv!r} - {r.exact!r}| = {err:.3e} > {tol:.3e}"
+    assert err <= tol, f"{dtype} {op} n={r.count}: |{gv!r} - {r.exact!r}| = {err:.3e} > {tol:.3e}"
     return r
 
 

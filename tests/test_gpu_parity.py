@@ -592,3 +592,56 @@ def test_fused_exchange_mismatch_and_timeout(rd):
         torch.cuda.synchronize()
         for c in comms:
             c.destroy()
+
+
+# ------------------------------------------------------------------ every pair at BASELINE's 2^28
+@pytest.mark.parametrize("dtype,op", PAIRS, ids=[f"{d}-{o}" for d, o in PAIRS])
+def test_all_pairs_full_size_2_28(rd, dtype, op):
+    """Each (dtype, op) at n = 2^28 through `reduce` (the AUTO planner picks the
+    bulk-copy kernel bench.py times) vs the oracle on the whole array."""
+    n = 1 << 28
+    x = _device_input(n, dtype, inputs.default_workload(dtype, op), 7)
+    g = val(rd.reduce(x, op))
+    assert rd.reduce_ex(x, op)[1]["variant"] == "bulk"
+    xh = x.cpu().numpy()
+    del x
+    _parity.check(g, xh, op)
+
+
+def _oracle_stream(x_dev, op, chunk=1 << 28):
+    """The oracle's left fold streamed over device chunks (fold(A); fold(B) ==
+    fold(A ++ B), pinned in test_streaming_fold_equals_one_shot)."""
+    f = oracle.Fold(str(x_dev.dtype).replace("torch.", ""), op)
+    for s in range(0, x_dev.numel(), chunk):
+        f.fold(x_dev[s:s + chunk].cpu().numpy())
+    return f.result()
+
+
+@pytest.mark.slow
+def test_c5_full_size_2_34(rd):
+    """BASELINE configs[4] at its real size on ONE GPU: n = 2^34 float32 (64 GiB
+    of HBM), sum and max; the whole array in one call, and the 8-way shard
+    layout through records. argmax exercises element indices >= 2^32."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < (70 << 30):
+        pytest.skip("needs 70 GiB of free HBM")
+    n = 1 << 34
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    for op, wl in (("max", "planted"), ("sum", "u01"), ("argmax", "planted")):
+        inputs.fill_device(x, wl, seed=1)
+        whole = val(rd.reduce(x, op))
+        recs = torch.empty(8 * 32, dtype=torch.uint8, device="cuda")
+        for r in range(8):
+            b, c = rd.shard_range(n, 8, r)
+            rd.reduce_partial(x[b:b + c], op, rec=recs[r * 32:(r + 1) * 32])
+        sharded = val(rd.combine_records(recs, "float32", op))
+        if op == "max":
+            assert float(whole) == float(sharded) == 2.0 ** 20
+        elif op == "argmax":
+            pmax, _ = inputs.planted_positions(1, n)
+            assert whole == sharded == (np.float32(2.0 ** 20), pmax)
+        else:
+            ref = _oracle_stream(x, "sum")
+            _parity.check(whole, np.zeros(0, np.float32), "sum", ref=ref)
+            _parity.check(sharded, np.zeros(0, np.float32), "sum", ref=ref)
+    del x

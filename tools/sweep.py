@@ -256,15 +256,69 @@ def do_crossover(args):
     return rows
 
 
+def do_multi(args):
+    """Step latency of the exchange paths at one rank (what a 1-GPU box can
+    measure): plain reduce vs reduce_multi (NCCL all-gather + combine kernel)
+    vs reduce_fused (exchange inside the kernel), K back-to-back calls."""
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29544")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    comm = rd.Comm.from_process_group()
+    fused = rd.FusedComm.from_process_group()
+    rows = []
+    for log2n in (10, 16, 20, 24, 28):
+        n = 1 << log2n
+        x = make(n, "float32", "u01")
+        paths = {"reduce": lambda: rd.reduce(x, "sum"),
+                 "reduce_multi_nccl": lambda: comm.reduce(x, "sum"),
+                 "reduce_fused": lambda: fused.reduce(x, "sum")}
+        for name, fn in paths.items():
+            for _ in range(10):
+                fn()
+            torch.cuda.synchronize()
+            s = torch.cuda.current_stream()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            K = 200
+            a.record(s)
+            for _ in range(K):
+                fn()
+            b.record(s)
+            b.synchronize()
+            us = a.elapsed_time(b) * 1e3 / K
+            # graph-captured (GPU-side latency without host launch overhead)
+            gs = torch.cuda.Stream()
+            with torch.cuda.stream(gs):
+                fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(20):
+                    fn()
+            g.replay()
+            torch.cuda.synchronize()
+            c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c.record(s)
+            g.replay()
+            d.record(s)
+            d.synchronize()
+            r = {"n": n, "path": name, "us_per_step": us, "graph_us_per_step": c.elapsed_time(d) * 1e3 / 20}
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+        fused.check()
+        comm.check()
+    return rows
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover"])
+    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
     args = p.parse_args()
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
-           "grids": do_grids, "crossover": do_crossover}[args.what](args)
+           "grids": do_grids, "crossover": do_crossover, "multi": do_multi}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
         json.dump({"meta": meta, "result": res}, f, indent=1)
