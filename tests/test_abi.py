@@ -130,3 +130,18 @@ def test_shard_range_partitions(n, W):
     assert max(sizes) - min(sizes) <= 1
     with pytest.raises(rd.ReduceError):
         rd.shard_range(n, W, W)
+
+
+def test_header_is_plain_c_and_links(tmp_path):
+    """include/b200reduce.h compiles as C99 (no C++ in the ABI) and a C program
+    links against libb200reduce.so (examples/reduce_example.c)."""
+    import subprocess
+    exe = tmp_path / "reduce_example"
+    cmd = ["gcc", "-std=c99", "-Wall", "-Werror", "-O2", os.path.join(ROOT, "examples", "reduce_example.c"),
+           "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           "-L", os.path.join(ROOT, "paper_1710_07358_b200"), "-lb200reduce",
+           f"-Wl,-rpath,{os.path.join(ROOT, 'paper_1710_07358_b200')}",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-o", str(exe)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert exe.exists()

@@ -645,3 +645,21 @@ def test_c5_full_size_2_34(rd):
             _parity.check(whole, np.zeros(0, np.float32), "sum", ref=ref)
             _parity.check(sharded, np.zeros(0, np.float32), "sum", ref=ref)
     del x
+
+
+def test_c_program_through_the_abi(rd, tmp_path):
+    """A plain C99 program (examples/reduce_example.c) drives the library: exact
+    sum of ones, argmax tie -> index 0, and back-to-back reduce() calls."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "reduce_example"
+    subprocess.check_call(["gcc", "-std=c99", "-O2", os.path.join(root, "examples", "reduce_example.c"),
+                           "-I", os.path.join(root, "include"), "-I", "/usr/local/cuda/include",
+                           "-L", os.path.join(root, "paper_1710_07358_b200"), "-lb200reduce",
+                           f"-Wl,-rpath,{os.path.join(root, 'paper_1710_07358_b200')}",
+                           "-L", "/usr/local/cuda/lib64", "-lcudart", "-o", str(exe)])
+    for log2n in ("10", "24"):
+        r = subprocess.run([str(exe), log2n], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stdout + r.stderr
+        print(r.stdout)

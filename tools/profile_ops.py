@@ -1,0 +1,27 @@
+#!/usr/bin/env python
+"""One reduce per selected (dtype, op) at n = 2^28, for an ncu capture:
+
+    ncu --set full -k regex:rd_ -o prof python tools/profile_ops.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+import paper_1710_07358_b200 as rd  # noqa: E402
+
+PAIRS = [("int32", "sum"), ("float64", "sum"), ("float64", "prod"), ("float32", "max"),
+         ("float32", "argmin"), ("float64", "sum_compensated")]
+
+if __name__ == "__main__":
+    n = 1 << 28
+    for dtype, op in PAIRS:
+        x = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
+        inputs.fill_device(x, inputs.default_workload(dtype, op), seed=1)
+        rd.reduce(x, op)
+        torch.cuda.synchronize()
+        del x
+    print("ok")
