@@ -128,7 +128,7 @@ def reduce_partial(x, op: str, rec=None, stream=None):
 def combine_records(recs, dtype, op: str, out=None, rec_out=None, status=None, stream=None):
     """Fold k records (a uint8 CUDA tensor of k*32 bytes) in index order."""
     torch = _torch()
-    name = _dtype_name(dtype)
+    name = _dtype_name(dtype)   # accepts a torch dtype or its name
     tdt = getattr(torch, name)
     if recs.numel() % RECORD_BYTES:
         raise ValueError("recs must hold whole 32-byte records")
@@ -147,8 +147,8 @@ def combine_records(recs, dtype, op: str, out=None, rec_out=None, status=None, s
 
 def reduce_host(x, op: str):
     """End-to-end reduction of a host array (numpy array or CPU tensor; pinned
-    memory gives overlapped copies). Returns a numpy scalar."""
-    torch = _torch()
+    memory gives overlapped copies). Returns a numpy scalar ((value, index)
+    for argmin / argmax)."""
     if isinstance(x, np.ndarray):
         arr = np.ascontiguousarray(x)
         name, ptr, n = arr.dtype.name, arr.ctypes.data, arr.size
@@ -167,7 +167,6 @@ def reduce_host(x, op: str):
     out = np.zeros(1, dtype=np.dtype(name))
     check(lib().reduce_host(ptr if n else None, n, DTYPE_NAMES[name], _op(op), out.ctypes.data),
           "reduce_host")
-    del torch
     return out[0]
 
 

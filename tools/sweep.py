@@ -126,15 +126,14 @@ def do_ablation(args):
             if args.only:
                 cfgs = [c for c in cfgs if c[0] in args.only]
             for variant, u, vb in cfgs:
-                if True:
-                        _, info = rd.reduce_ex(x, "sum", variant=variant, unroll=u, vec_bytes=vb, out=o)
-                        fn = lambda: rd.reduce_ex(x, "sum", variant=variant, unroll=u, vec_bytes=vb, out=o)
-                        r = time_launch(fn, n * 4)
-                        r.update({"variant": variant, "unroll": u, "vec_bytes": info["vec_bytes"],
-                                  "grid": info["grid"], "regs": info["regs_per_thread"],
-                                  "ctas_per_sm": info["ctas_per_sm"]})
-                        rows.append(r)
-                        print(dtype, n, json.dumps(r), flush=True)
+                _, info = rd.reduce_ex(x, "sum", variant=variant, unroll=u, vec_bytes=vb, out=o)
+                fn = lambda: rd.reduce_ex(x, "sum", variant=variant, unroll=u, vec_bytes=vb, out=o)
+                r = time_launch(fn, n * 4)
+                r.update({"variant": variant, "unroll": u, "vec_bytes": info["vec_bytes"],
+                          "grid": info["grid"], "regs": info["regs_per_thread"],
+                          "ctas_per_sm": info["ctas_per_sm"]})
+                rows.append(r)
+                print(dtype, n, json.dumps(r), flush=True)
             out[f"{dtype}-{n}"] = rows
             del x
     return out
