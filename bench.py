@@ -187,10 +187,34 @@ def run_b200(args):
     x = torch.empty(n, dtype=getattr(torch, dt), device=dev)
     inputs.fill_device(x, wl, seed=1, offset=rank * n, n_total=n * ws)
     out = torch.empty((), dtype=x.dtype, device=dev)
-    if use_comm and args.fused:
-        comm = rd.FusedComm.from_process_group()     # exchange fused into the reduce kernel (f1)
-    else:
-        comm = rd.Comm.from_process_group() if use_comm else None
+    comm = rd.Comm.from_process_group() if use_comm else None   # NCCL all-gather exchange
+    exchange = "nccl"
+    if use_comm and args.exchange == "fused":
+        # the exchange fused into the reduce kernel, verified against
+        # the NCCL path on this data before it is timed: both fold the same W
+        # records in rank order, so the bits must agree on every rank
+        import torch.distributed as dist
+        ok = torch.zeros(1, device=dev)
+        fused = None
+        try:
+            fused = rd.FusedComm.from_process_group()
+            a_f = fused.reduce(x, op)
+            a_n = comm.reduce(x, op)
+            fused.check()
+            comm.check()
+            pairs = zip(a_f, a_n) if op in rd.ARG_OPS else [(a_f, a_n)]
+            same = all(bool((u.reshape(1).view(torch.uint8) == v.reshape(1).view(torch.uint8)).all().item())
+                       for u, v in pairs)
+            ok.fill_(1.0 if same else 0.0)
+        except Exception as e:  # IPC unavailable, timeout, mismatch: keep NCCL
+            print(f"[bench] fused exchange unavailable on rank {rank}: {e}", file=sys.stderr)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 1.0:
+            comm.destroy()
+            comm, exchange = fused, "fused"
+        elif fused is not None:
+            torch.cuda.synchronize(dev)
+            fused.destroy()
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -348,8 +372,8 @@ def run_b200(args):
                        "n_per_gpu": n, "n_total": n * ws, "op": op,
                        "l2": "input (%.2f GB/GPU) > 126 MB L2: no flush" % (n * s / 1e9),
                        "parallelism": f"shard{ws}" if ws > 1 else "single",
-                       "exchange": ("fused in-kernel (reduce_fused)" if args.fused else "NCCL all-gather (reduce_multi)")
-                       if use_comm else None},
+                       "exchange": ("fused in-kernel over NVLink (reduce_fused)" if exchange == "fused"
+                                    else "NCCL all-gather + rank-order fold (reduce_multi)") if use_comm else None},
             "pct_hbm_peak": round(100 * value / (peak * ws), 2),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
@@ -359,7 +383,7 @@ def run_b200(args):
                          "algorithmic_bytes_per_launch": n * s},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": K * (1 if (comm is None or args.fused) else 2),
+            "gpu_launches": K * (1 if (comm is None or exchange == "fused") else 2),
             "clocks": clocks,
             "context": {"torch_sum_gbs": tctx, "result": res},
         }
@@ -383,8 +407,9 @@ def main():
     p.add_argument("--log2n", type=int, default=28)
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--fused", action="store_true",
-                   help="N>1: exchange partials inside the reduce kernel over NVLink (reduce_fused) instead of NCCL")
+    p.add_argument("--exchange", choices=["fused", "nccl"], default="fused",
+                   help="N>1: exchange partials inside the reduce kernel over NVLink (reduce_fused, verified "
+                        "against NCCL first, falls back to it) or with an NCCL all-gather (reduce_multi)")
     p.add_argument("--force-comm", action="store_true",
                    help="use the reduce_multi (NCCL) step even at one rank (tests the N>1 path on one GPU)")
     p.add_argument("--profile", action="store_true",
