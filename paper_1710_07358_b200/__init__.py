@@ -46,11 +46,17 @@ def _dtype_name(dt) -> str:
     return s.replace("torch.", "")
 
 
+_DT_CACHE = {}
+
+
 def _dt(t) -> int:
-    name = _dtype_name(t.dtype)
-    if name not in DTYPE_NAMES:
-        raise TypeError(f"unsupported dtype {t.dtype}")
-    return DTYPE_NAMES[name]
+    code = _DT_CACHE.get(t.dtype)
+    if code is None:
+        name = _dtype_name(t.dtype)
+        if name not in DTYPE_NAMES:
+            raise TypeError(f"unsupported dtype {t.dtype}")
+        code = _DT_CACHE[t.dtype] = DTYPE_NAMES[name]
+    return code
 
 
 def _op(op: str) -> int:
@@ -60,8 +66,11 @@ def _op(op: str) -> int:
 
 
 def _stream(t, stream):
-    torch = _torch()
     if stream is None:
+        torch = _torch()
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:
+            return raw(t.device.index)
         return torch.cuda.current_stream(t.device).cuda_stream
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 

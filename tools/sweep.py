@@ -309,15 +309,37 @@ def do_multi(args):
     return rows
 
 
+def do_overhead(args):
+    """Host cost per call of the Python binding vs the C ABI (tiny n, back to back)."""
+    rows = []
+    x = make(1024, "float32", "u01")
+    o = torch.empty((), dtype=torch.float32, device="cuda")
+    import time as _t
+    for name, fn in (("python reduce(x, op)", lambda: rd.reduce(x, "sum")),
+                     ("python reduce(x, op, out=o)", lambda: rd.reduce(x, "sum", out=o))):
+        for _ in range(100):
+            fn()
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        for _ in range(2000):
+            fn()
+        torch.cuda.synchronize()
+        r = {"path": name, "us_per_call": (_t.perf_counter() - t0) / 2000 * 1e6}
+        rows.append(r)
+        print(json.dumps(r), flush=True)
+    return rows
+
+
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi"])
+    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi", "overhead"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
     args = p.parse_args()
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
-           "grids": do_grids, "crossover": do_crossover, "multi": do_multi}[args.what](args)
+           "grids": do_grids, "crossover": do_crossover, "multi": do_multi,
+           "overhead": do_overhead}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
         json.dump({"meta": meta, "result": res}, f, indent=1)
