@@ -663,3 +663,62 @@ def test_c_program_through_the_abi(rd, tmp_path):
         r = subprocess.run([str(exe), log2n], capture_output=True, text=True, timeout=120)
         assert r.returncode == 0, r.stdout + r.stderr
         print(r.stdout)
+
+
+def test_cuda_graph_capture_bulk_and_args(rd):
+    """The bulk-copy kernel (>= 128 MiB), an arg op and a shard record, captured
+    in one CUDA graph and replayed twice."""
+    n = (1 << 25) + 3                         # 128 MiB + 12 B of float32 -> bulk
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    inputs.fill_device(x, "u01", seed=8)
+    s = torch.cuda.Stream()
+    out = torch.empty((), dtype=torch.float32, device="cuda")
+    arg = torch.empty(2, dtype=torch.int64, device="cuda")
+    rec = torch.empty(32, dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(s):
+        assert rd.reduce_ex(x, "sum", out=out)[1]["variant"] == "bulk"
+        rd.reduce(x, "argmax", out=arg)
+        rd.reduce_partial(x[1:], "max", rec=rec)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        rd.reduce(x, "sum", out=out)
+        rd.reduce(x, "argmax", out=arg)
+        rd.reduce_partial(x[1:], "max", rec=rec)
+    xh = x.cpu().numpy()
+    for _ in range(2):
+        out.zero_()
+        arg.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        _parity.check(val(out), xh, "sum")
+        _parity.check(val(rd._arg_view(arg, torch.float32)), xh, "argmax")
+        _parity.check(val(rd.combine_records(rec, "float32", "max")), xh[1:], "max")
+
+
+def test_host_threads_concurrently(rd):
+    """Several host threads, each with its own stream, call the library at once
+    (ctypes releases the GIL; the workspace map is locked)."""
+    import threading
+    xs = [inputs.generate((1 << 20) + 17 * i, "int64", "uniform_bits", seed=i + 1) for i in range(6)]
+    ds = [to_dev(x, i % 3) for i, x in enumerate(xs)]
+    errors = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(40):
+                    o = rd.reduce(ds[i], "sum" if rep % 2 else "xor")
+                    if rep % 10 == 9:
+                        s.synchronize()
+                        _parity.check(val(o), xs[i], "sum" if rep % 2 else "xor")
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(xs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
