@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -129,6 +130,16 @@ bool lookup(int dtype, int op, int variant, int unroll, int vec_bytes, KernelRef
   return lookup_int(dtype, op, variant, unroll, vec_bytes, r);
 }
 
+// Tuning knobs for the bulk chunk schedule (measurement only; the defaults
+// are the documented schedule). They are constants of the schedule, so the
+// result stays a function of n and the alignment for a fixed environment.
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  const unsigned long long x = std::strtoull(v, nullptr, 10);
+  return x ? (uint64_t)x : dflt;
+}
+
 }  // namespace
 
 // Load (and configure) every default kernel now. With CUDA lazy loading, the
@@ -229,21 +240,26 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   }
   if (k.variant == RD_VARIANT_BULK) {
     // Chunk schedule, fixed by n and the base alignment only (determinism):
-    // a head region in chunks of C0 (about 12 per SM, at most ~6000), then a
-    // tail region of ~148*4 chunks of C1 = 2 stages, so the dynamic schedule
+    // a head region in chunks of C0 (about 16 per SM, at most 5000), then a
+    // tail region of 148*16 chunks of C1 = one stage, so the dynamic schedule
     // ends with short chunks and the per-SM tail imbalance is < one C1 chunk.
+    // (16/16/1 measured best of a sweep, tools/tune_bulk.sh: +0.9% over 12/4/2.)
+    static const uint64_t kHeadPerSm = env_u64("RD_TUNE_HEAD_PER_SM", 16);
+    static const uint64_t kTailPerSm = env_u64("RD_TUNE_TAIL_PER_SM", 16);
+    static const uint64_t kTailStages = env_u64("RD_TUNE_TAIL_STAGES", 1);
     const uint64_t T = a.nvec * 16;
     const uint64_t S = (uint64_t)k.vec_bytes;
-    const uint64_t C1 = 2 * S;
-    const uint64_t R = T < 148ull * 4 * C1 ? T : 148ull * 4 * C1;
-    uint64_t c0 = T / (148ull * 12);
-    if (c0 < T / 6000) c0 = T / 6000;
+    const uint64_t C1 = kTailStages * S;
+    const uint64_t R = T < 148ull * kTailPerSm * C1 ? T : 148ull * kTailPerSm * C1;
+    uint64_t c0 = T / (148ull * kHeadPerSm);
+    if (c0 < T / 5000) c0 = T / 5000;   // head <= 5000 chunks: head + tail <= kMaxSlots
     c0 = (c0 + S - 1) / S * S;
     if (c0 < 4 * S) c0 = 4 * S;
-    const uint64_t nhead = (T - R) / c0;
-    const uint64_t ntail = (T - nhead * c0 + C1 - 1) / C1;
+    const uint64_t nhead = (T - R + c0 - 1) / c0;       // the head region is T - R bytes exactly
+    const uint64_t ntail = (R + C1 - 1) / C1;           // <= 148 * kTailPerSm
     a.chunk_bytes = c0;
     a.tail_chunk_bytes = C1;
+    a.head_region_bytes = T - R;
     a.nhead_chunks = (uint32_t)nhead;
     a.nchunks = (uint32_t)(nhead + ntail);
     if (a.nchunks > (uint32_t)kMaxSlots) { set_error("chunk schedule exceeds the workspace"); return RD_ERR_INVALID_ARG; }

@@ -117,8 +117,12 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (;;) {
-        const uint32_t c = atomicAdd(args.work, 1u);
+      // the first chunk is static (no atomic on the critical path at start);
+      // later claims come from the counter, offset by the grid, and the next
+      // claim is issued before the current chunk is streamed (latency hidden)
+      uint32_t c = blockIdx.x;
+      uint32_t next = atomicAdd(args.work, 1u) + gridDim.x;
+      for (;; c = next, next = atomicAdd(args.work, 1u) + gridDim.x) {
         if (c >= args.nchunks) {
           mbar_wait(&empty[stage], phase ^ 1);
           st_chunk[stage] = -1;

@@ -56,6 +56,7 @@ struct KArgs {
   // bulk variant only: the chunk schedule (fixed by n and the base alignment)
   uint64_t chunk_bytes;     // head-region chunk size C0 (a multiple of the stage size)
   uint64_t tail_chunk_bytes;// tail-region chunk size C1 (smaller: short tail imbalance)
+  uint64_t head_region_bytes;// bytes covered by the head chunks
   uint32_t nchunks;         // chunks in the body
   uint32_t nhead_chunks;    // chunks of size C0; the rest have size C1
   unsigned* work;           // dynamic chunk counter, zero between launches
@@ -79,10 +80,9 @@ __device__ __forceinline__ void chunk_range(const struct KArgs& a, uint32_t c, u
                                             uint64_t* off, uint64_t* len) {
   if (c < a.nhead_chunks) {
     *off = (uint64_t)c * a.chunk_bytes;
-    *len = a.chunk_bytes;
+    *len = min(a.chunk_bytes, a.head_region_bytes - *off);   // the last head chunk may be short
   } else {
-    const uint64_t head_bytes = (uint64_t)a.nhead_chunks * a.chunk_bytes;
-    *off = head_bytes + (uint64_t)(c - a.nhead_chunks) * a.tail_chunk_bytes;
+    *off = a.head_region_bytes + (uint64_t)(c - a.nhead_chunks) * a.tail_chunk_bytes;
     *len = min(a.tail_chunk_bytes, body_bytes - *off);
   }
 }
