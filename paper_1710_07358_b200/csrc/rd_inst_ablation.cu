@@ -38,6 +38,8 @@ bool lookup_sweep(int variant, int unroll, int vec_bytes, KernelRef* r) {
     const int st = unroll ? unroll : kBulkStages;
     const int sb = vec_bytes ? vec_bytes : kBulkStageBytes;
     return bulk_entry<OpT, 4, 32768>(st, sb, r) || bulk_entry<OpT, 6, 32768>(st, sb, r) ||
+           bulk_entry<OpT, 3, 32768>(st, sb, r) || bulk_entry<OpT, 5, 32768>(st, sb, r) ||
+           bulk_entry<OpT, 2, 65536>(st, sb, r) || bulk_entry<OpT, 4, 49152>(st, sb, r) ||
            bulk_entry<OpT, 3, 65536>(st, sb, r) || bulk_entry<OpT, 12, 16384>(st, sb, r) ||
            bulk_entry<OpT, 8, 16384>(st, sb, r) || bulk_entry<OpT, 6, 16384>(st, sb, r) ||
            bulk_entry<OpT, 24, 8192>(st, sb, r);

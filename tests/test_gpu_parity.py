@@ -140,7 +140,8 @@ def test_ablation_configs(rd, dtype):
             _parity.check(val(out), x, "sum")
 
 
-BULK_CONFIGS = [(4, 32768), (6, 32768), (3, 65536), (12, 16384), (8, 16384), (6, 16384), (24, 8192)]
+BULK_CONFIGS = [(4, 32768), (6, 32768), (3, 65536), (12, 16384), (8, 16384), (6, 16384), (24, 8192),
+                (3, 32768), (5, 32768), (2, 65536), (4, 49152)]
 
 
 @pytest.mark.parametrize("dtype", ["float32", "int32"])

@@ -122,7 +122,8 @@ def do_ablation(args):
             cfgs = [("vector", u, vb) for vb in (4, 8, 16, 32) for u in (1, 2, 3, 4, 5, 6, 7, 8, 16)]
             cfgs += [("paper", u, 0) for u in (1, 2, 3, 4, 5, 6, 7, 8, 16)]
             cfgs += [("bulk", st, sb) for st, sb in ((4, 32768), (6, 32768), (3, 65536), (12, 16384),
-                                                     (8, 16384), (6, 16384), (24, 8192))]
+                                                     (8, 16384), (6, 16384), (24, 8192), (3, 32768),
+                                                     (5, 32768), (2, 65536), (4, 49152))]
             if args.only:
                 cfgs = [c for c in cfgs if c[0] in args.only]
             for variant, u, vb in cfgs:
