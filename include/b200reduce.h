@@ -144,8 +144,9 @@ rd_status reduce_partial(const void* x, size_t n, rd_dtype dtype, rd_op op, rd_r
  * (dtype, op), *d_status (a device int, may be NULL) is set to
  * RD_ERR_MISMATCH and `out` receives the empty result.
  * The "second stage" of P:180 applied across blocks held by different
- * owners. Errors: INVALID_ARG (recs NULL with count > 0, count < 0, both
- * outputs NULL), UNSUPPORTED, CUDA. */
+ * owners. One warp: records are loaded 32 at a time and folded sequentially.
+ * Errors: INVALID_ARG (recs NULL with count > 0, count < 0, both outputs
+ * NULL), MISALIGNED (recs not 16-byte aligned), UNSUPPORTED, CUDA. */
 rd_status rd_combine_records(const rd_record* recs, int count, rd_dtype dtype, rd_op op,
                              void* out, rd_record* rec_out, int* d_status, rd_stream_t stream);
 

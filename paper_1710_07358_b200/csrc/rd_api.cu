@@ -330,6 +330,7 @@ rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, vo
   rd_status st = check_dtype_op(dtype, op);
   if (st != RD_OK) return st;
   if (count < 0 || (count > 0 && recs == nullptr)) { set_error("bad recs/count"); return RD_ERR_INVALID_ARG; }
+  if ((uintptr_t)recs % 16) { set_error("recs must be 16-byte aligned"); return RD_ERR_MISALIGNED; }
   if (out == nullptr && rec_out == nullptr) { set_error("no output"); return RD_ERR_INVALID_ARG; }
   if (out && (uintptr_t)out % (is_arg_op(op) ? 8 : dtype_size(dtype))) { set_error("out misaligned"); return RD_ERR_MISALIGNED; }
   CombineFn fn = lookup_combine(dtype, op);

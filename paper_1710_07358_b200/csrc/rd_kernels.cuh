@@ -33,9 +33,12 @@ namespace rd {
 // reduction ahead of a peer (it cannot finish epoch e+1 before that peer has
 // sent its e+1 record, which the peer does only after folding epoch e).
 constexpr int kMaxRanks = 32;
+// Records travel in "LL" form (NCCL's low-latency idea): each 8-byte word holds
+// 4 bytes of the 32-byte record and the 32-bit epoch, and is written with one
+// single-copy-atomic 8-byte store. A reader polls the 8 words until all carry
+// the expected epoch -- no fences, no release/acquire round trips.
 struct Mailbox {
-  rd_record rec[2][kMaxRanks];
-  unsigned long long flag[2][kMaxRanks];   // epoch of the record in rec[par][sender]
+  unsigned long long ll[2][kMaxRanks][8];  // [epoch parity][sender][word]
   unsigned long long epoch;                // calls completed by this rank (device-side:
                                            // the exchange is CUDA-graph capturable)
 };
@@ -166,21 +169,43 @@ __device__ __forceinline__ void finish(const typename OpT::Acc& a, const KArgs& 
   }
 }
 
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
+// Fold `count` records in INDEX order with one warp: lanes load 32 records at
+// a time in parallel (one memory round trip per 32), then every lane folds
+// them sequentially from shuffles (same order, same result in every lane).
+// Indexed ops shift each record's indices by the n of the records before it.
+template <class OpT, class Load>
+__device__ __forceinline__ void fold_records_warp(int count, uint32_t tag, Load load, typename OpT::Acc* acc_out,
+                                                  uint64_t* n_out, bool* bad_out) {
+  using Acc = typename OpT::Acc;
+  const int ln = threadIdx.x & 31;
+  Acc a = OpT::identity();
+  uint64_t n = 0;
+  bool bad = false;
+  for (int base = 0; base < count; base += 32) {
+    uint32_t t = 0;
+    uint64_t rn = 0, a0 = 0, a1 = 0;
+    if (base + ln < count) load(base + ln, &t, &rn, &a0, &a1);
+    const int m = min(32, count - base);
+    for (int j = 0; j < m; ++j) {
+      const uint32_t tj = __shfl_sync(0xffffffffu, t, j);
+      const uint64_t nj = shfl_idx_u64(rn, j), x0 = shfl_idx_u64(a0, j), x1 = shfl_idx_u64(a1, j);
+      if (tj != tag) { bad = true; continue; }
+      a = OpT::combine(a, shifted<OpT>(OpT::unpack(Slot{x0, x1}), n));
+      n += nj;
+    }
+  }
+  *acc_out = a;
+  *n_out = n;
+  *bad_out = bad;
 }
 
 // a8 fused into the kernel: warp 0 of the last CTA pushes this
 // rank's record into slot [epoch&1][rank] of every peer's mailbox (peer
-// stores over NVLink), publishes it with a system-scope release of the
-// epoch, waits for the W records of this epoch in its own mailbox, and folds
-// them in RANK ORDER -- every rank computes the identical result, with no
-// host call and no second kernel. A bounded wait reports RD_ERR_TIMEOUT.
+// stores over NVLink) as 8 self-validating 8-byte words {payload, epoch},
+// polls its own mailbox until the W records of this epoch are complete, and
+// folds them in RANK ORDER -- every rank computes the identical result, with
+// no host call, no second kernel and no memory fence. A bounded wait reports
+// RD_ERR_TIMEOUT.
 template <class OpT>
 __device__ __noinline__ void fused_exchange(typename OpT::Acc a, const KArgs& args) {
   const int ln = threadIdx.x & 31;
@@ -191,42 +216,48 @@ __device__ __noinline__ void fused_exchange(typename OpT::Acc a, const KArgs& ar
   // its own mailbox is read and bumped without races
   const unsigned long long epoch = *(volatile unsigned long long*)&args.self->epoch + 1;
   const int par = (int)(epoch & 1);
+  const unsigned long long eflag = (unsigned long long)(uint32_t)epoch << 32;
   const int W = args.nranks;
+  // the record as 8 x 32-bit payload words: {tag, status=0, n lo, n hi, a lo, a hi, b lo, b hi}
+  uint32_t w[8] = {args.tag, 0u, (uint32_t)args.n, (uint32_t)(args.n >> 32),
+                   (uint32_t)s.a, (uint32_t)(s.a >> 32), (uint32_t)s.b, (uint32_t)(s.b >> 32)};
   for (int p = ln; p < W; p += 32) {
-    Mailbox* dst = args.peers[p];
-    volatile unsigned long long* r = reinterpret_cast<volatile unsigned long long*>(&dst->rec[par][args.rank]);
-    r[0] = (unsigned long long)args.tag;               // tag (low 32) | status 0 (high 32)
-    r[1] = args.n;
-    r[2] = s.a;
-    r[3] = s.b;
-    // the release orders the record stores above before the flag (no full fence)
-    st_release_sys(&dst->flag[par][args.rank], epoch);
+    volatile unsigned long long* dst = args.peers[p]->ll[par][args.rank];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[k] = eflag | w[k];   // peer store over NVLink (or local)
   }
   bool timeout = false;
+  uint32_t got[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int q = ln; q < W; q += 32) {
+    const volatile unsigned long long* src = args.self->ll[par][q];
     uint32_t spins = 0;
-    while (ld_acquire_sys(&args.self->flag[par][q]) != epoch) {
+    for (;;) {
+      bool all = true;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const unsigned long long v = src[k];
+        got[k] = (uint32_t)v;
+        all = all && ((v & 0xffffffff00000000ull) == eflag);
+      }
+      if (all) break;
       if (++spins > 4096) __nanosleep(128);           // tight spin first, then back off
       if (spins > (1u << 25)) { timeout = true; break; }
     }
+  }  timeout = __any_sync(0xffffffffu, timeout);
+  using Acc = typename OpT::Acc;
+  Acc acc = OpT::identity();
+  uint64_t nn = 0;
+  bool bad = false;
+  if (!timeout) {
+    // lane q already holds record q (its 8 payload words)
+    fold_records_warp<OpT>(W, args.tag, [&](int, uint32_t* t, uint64_t* n, uint64_t* a0, uint64_t* a1) {
+      *t = got[0];
+      *n = ((uint64_t)got[3] << 32) | got[2];
+      *a0 = ((uint64_t)got[5] << 32) | got[4];
+      *a1 = ((uint64_t)got[7] << 32) | got[6];
+    }, &acc, &nn, &bad);
   }
-  timeout = __any_sync(0xffffffffu, timeout);
   if (ln == 0) {
-    using Acc = typename OpT::Acc;
-    Acc acc = OpT::identity();
-    uint64_t nn = 0;
-    bool bad = false;
-    for (int q = 0; q < W && !timeout; ++q) {
-      (void)ld_acquire_sys(&args.self->flag[par][q]);  // acquire in this thread too
-      const volatile unsigned long long* r =
-          reinterpret_cast<const volatile unsigned long long*>(&args.self->rec[par][q]);
-      const uint32_t tag = (uint32_t)r[0];
-      const uint64_t n = r[1];
-      const Slot sl{r[2], r[3]};
-      if (tag != args.tag) { bad = true; continue; }
-      acc = OpT::combine(acc, shifted<OpT>(OpT::unpack(sl), nn));
-      nn += n;
-    }
     if (timeout) atomicExch(args.err, (int)RD_ERR_TIMEOUT);
     else if (bad) atomicExch(args.err, (int)RD_ERR_MISMATCH);
     if (timeout || bad || nn == 0) OpT::store_empty(args.out);
@@ -377,18 +408,20 @@ __global__ void __launch_bounds__(B) rd_paper_kernel(const KArgs args) {
 template <class OpT>
 __global__ void rd_combine_kernel(const rd_record* recs, int count, uint32_t tag, void* out,
                                   rd_record* rec_out, int* d_status) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (blockIdx.x != 0 || threadIdx.x >= 32) return;
   using Acc = typename OpT::Acc;
-  Acc a = OpT::identity();
-  uint64_t n = 0;
-  bool bad = false;
-  for (int r = 0; r < count; ++r) {
-    const rd_record rc = recs[r];
-    if (rc.tag != tag) { bad = true; continue; }
-    // record r covers the block after the previous ones: indices shift by n so far
-    a = OpT::combine(a, shifted<OpT>(OpT::unpack(Slot{rc.acc[0], rc.acc[1]}), n));
-    n += rc.n;
-  }
+  Acc a;
+  uint64_t n;
+  bool bad;
+  fold_records_warp<OpT>(count, tag, [&](int r, uint32_t* t, uint64_t* rn, uint64_t* a0, uint64_t* a1) {
+    const ulonglong2 h = __ldcg(reinterpret_cast<const ulonglong2*>(recs + r));       // {tag|status, n}
+    const ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2*>(recs + r) + 1);   // acc[0..1]
+    *t = (uint32_t)h.x;
+    *rn = h.y;
+    *a0 = v.x;
+    *a1 = v.y;
+  }, &a, &n, &bad);
+  if (threadIdx.x != 0) return;
   if (bad && d_status) *d_status = (int)RD_ERR_MISMATCH;
   if (out) {
     if (n == 0 || bad) OpT::store_empty(out);
