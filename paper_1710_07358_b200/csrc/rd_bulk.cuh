@@ -171,8 +171,10 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
 #pragma unroll
         for (int k = 0; k < PER_THREAD; ++k) {
           Vec<16> w{{v[k].x, v[k].y, v[k].z, v[k].w}};
+          T xs[L];
 #pragma unroll
-          for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, 16>(w, l), step0 + k);
+          for (int l = 0; l < L; ++l) xs[l] = lane<T, 16>(w, l);
+          LO::fold_vec(acc, xs, step0 + k);
         }
       } else {
 #pragma unroll
@@ -181,8 +183,10 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
           if (off < bytes) {
             uint4 q = lds128(base + off);
             Vec<16> w{{q.x, q.y, q.z, q.w}};
+            T xs[L];
 #pragma unroll
-            for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, 16>(w, l), step0 + k);
+            for (int l = 0; l < L; ++l) xs[l] = lane<T, 16>(w, l);
+            LO::fold_vec(acc, xs, step0 + k);
           }
         }
       }
@@ -200,12 +204,9 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
         uint64_t coff = 0, clen = 0;
         if constexpr (OpT::kIndexed) chunk_range(args, (uint32_t)c, body_bytes, &coff, &clen);
         const uint64_t e_chunk = args.head + coff / sizeof(T);
-        Acc a = OpT::identity();
-#pragma unroll
-        for (int l = 0; l < L; ++l)
-          a = OpT::combine(a, LO::finish(acc[l], [&](uint32_t st) {
-                return e_chunk + ((uint64_t)(st / PER_THREAD) * (STAGE_BYTES / 16) + (st % PER_THREAD) * CT + t) * L + l;
-              }));
+        Acc a = LO::finish(acc, [&](uint32_t st, uint32_t ln) {
+          return e_chunk + ((uint64_t)(st / PER_THREAD) * (STAGE_BYTES / 16) + (st % PER_THREAD) * CT + t) * L + ln;
+        });
         a = OpT::warp_reduce(a);
         Acc* wp = wpart + (nchunk_local & 1) * CW;
         if (ln == 0) wp[warp] = a;

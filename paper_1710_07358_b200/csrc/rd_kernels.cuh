@@ -346,22 +346,24 @@ __global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < U; ++u) {
+        T xs[L];
 #pragma unroll
-        for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, VB>(v[u], l), step + u);
+        for (int l = 0; l < L; ++l) xs[l] = lane<T, VB>(v[u], l);
+        LO::fold_vec(acc, xs, step + u);
+      }
     }
   }
   for (; i < nvec; i += stride, ++step) {
     Vec<VB> v = ldg_stream<VB>(body + i * VB);
+    T xs[L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) acc[l] = LO::fold(acc[l], lane<T, VB>(v, l), step);
+    for (int l = 0; l < L; ++l) xs[l] = lane<T, VB>(v, l);
+    LO::fold_vec(acc, xs, step);
   }
   pdl_trigger();
-  // a3: lanes -> one accumulator (indexed ops: element index = head + (tid + step*stride)*L + l)
-  Acc a = OpT::identity();
-#pragma unroll
-  for (int l = 0; l < L; ++l)
-    a = OpT::combine(a, LO::finish(acc[l], [&](uint32_t st) { return args.head + (tid + (uint64_t)st * stride) * L + l; }));
+  // a3: lanes -> one accumulator (indexed ops: element index = head + (tid + step*stride)*L + lane)
+  Acc a = LO::finish(acc, [&](uint32_t st, uint32_t ln) { return args.head + (tid + (uint64_t)st * stride) * L + ln; });
   // a2: head and tail stragglers
   if (tid < args.head) a = fold_at<OpT>(a, ldg_scalar<T>(args.x + tid * sizeof(T)), tid);
   if (tid < args.tail)

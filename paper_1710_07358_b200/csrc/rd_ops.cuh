@@ -361,6 +361,15 @@ struct ArgOp {
       return nan ? (OP == RD_ARGMIN ? (U)0 : (U)~(U)0) : k;
     }
   }
+  // the order key without the NaN mapping (exact for every non-NaN element)
+  __device__ __forceinline__ static U raw_key(U b) {
+    if constexpr (DT == RD_UINT32) return b;
+    else if constexpr (!kFloat) return b ^ kSign;
+    else {
+      const U sgn = (U)((typename std::make_signed<U>::type)b >> (kBits - 1));
+      return b ^ (sgn | kSign);
+    }
+  }
   __device__ __forceinline__ static U bits_of(U k) {   // inverse of key_of (non-NaN)
     if constexpr (DT == RD_UINT32) return k;
     else if constexpr (!kFloat) return k ^ kSign;
@@ -428,18 +437,30 @@ __device__ __forceinline__ typename OpT::Acc shifted(typename OpT::Acc a, uint64
 #define OP_IS_MIN(OpT) (OpT::kMin)
 
 // ---------------------------------------------------------- lane accumulators
-// What the hot loops keep per (thread, vector lane). For plain ops it is the
-// op's accumulator. For indexed ops (argmin / argmax) it is the best order key
-// and the STEP at which it was seen: along one lane the element index grows
-// with the step, so a strict comparison keeps the earliest of equal keys and
-// the 64-bit global index is only formed once, in finish().
+// What the hot loops keep per thread. fold_vec folds one loaded vector (L
+// lanes, consecutive elements); finish combines the lanes into one Acc.
+// Plain ops keep one accumulator per lane (L independent dependency chains).
+// Indexed ops (argmin / argmax) keep per lane the best order key and the STEP
+// at which it was seen: along one lane the element index grows with the step,
+// so a strict comparison keeps the earliest of equal keys, and the 64-bit
+// index is formed once, in finish().
 template <class OpT, bool IDX = OpT::kIndexed>
 struct LaneOps {
+  using T = typename OpT::T;
   using Lane = typename OpT::Acc;
   __device__ __forceinline__ static Lane identity() { return OpT::identity(); }
-  __device__ __forceinline__ static Lane fold(Lane a, typename OpT::T x, uint32_t) { return OpT::fold(a, x); }
-  template <class F>
-  __device__ __forceinline__ static typename OpT::Acc finish(Lane a, F) { return a; }
+  template <int L>
+  __device__ __forceinline__ static void fold_vec(Lane (&acc)[L], const T (&x)[L], uint32_t) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], x[l]);
+  }
+  template <int L, class F>
+  __device__ __forceinline__ static typename OpT::Acc finish(const Lane (&acc)[L], F) {
+    typename OpT::Acc a = acc[0];
+#pragma unroll
+    for (int l = 1; l < L; ++l) a = OpT::combine(a, acc[l]);
+    return a;
+  }
 };
 
 template <class OpT>
@@ -448,18 +469,28 @@ struct LaneOps<OpT, true> {
   struct Lane { T key; uint32_t step; };
   static constexpr uint32_t kEmpty = 0xffffffffu;
   __device__ __forceinline__ static Lane identity() { return Lane{OpT::identity().key, kEmpty}; }
-  __device__ __forceinline__ static Lane fold(Lane a, T x, uint32_t step) {
-    const T k = OpT::key_of(x);
-    bool better = OP_IS_MIN(OpT) ? (k < a.key) : (k > a.key);
-    // float keys never reach the identity key; integer keys can, so an empty
-    // lane must take its first element unconditionally
-    if constexpr (!OpT::kFloat) better = better || (a.step == kEmpty);
-    return better ? Lane{k, step} : a;
+  template <int L>
+  __device__ __forceinline__ static void fold_vec(Lane (&acc)[L], const T (&x)[L], uint32_t step) {
+    // one (key, step) per lane: L independent branch-free chains. (A single
+    // per-thread accumulator with a per-vector early-out measured slower: the
+    // data-dependent branch costs more than the selects it saves.)
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const T k = OpT::key_of(x[l]);
+      bool better = OP_IS_MIN(OpT) ? (k < acc[l].key) : (k > acc[l].key);
+      // float keys never reach the identity key; integer keys can, so an empty
+      // lane must take its first element unconditionally
+      if constexpr (!OpT::kFloat) better = better || (acc[l].step == kEmpty);
+      acc[l] = better ? Lane{k, step} : acc[l];
+    }
   }
-  template <class F>
-  __device__ __forceinline__ static typename OpT::Acc finish(Lane a, F index_of) {
-    if (a.step == kEmpty) return OpT::identity();
-    return typename OpT::Acc{a.key, index_of(a.step)};
+  template <int L, class Fn>
+  __device__ __forceinline__ static typename OpT::Acc finish(const Lane (&acc)[L], Fn index_of) {
+    typename OpT::Acc a = OpT::identity();
+#pragma unroll
+    for (int l = 0; l < L; ++l)
+      if (acc[l].step != kEmpty) a = OpT::combine(a, typename OpT::Acc{acc[l].key, index_of(acc[l].step, (uint32_t)l)});
+    return a;
   }
 };
 
