@@ -55,7 +55,7 @@ struct KArgs {
   Slot* partials;           // gridDim.x slots (workspace)
   unsigned* ticket;         // zero between launches (workspace)
   uint32_t tag;             // record tag
-  int mode;                 // 0 = value, 1 = record
+  int mode;                 // 0 = value, 1 = record, 2 = fused multi-GPU exchange
   // bulk variant only: the chunk schedule (fixed by n and the base alignment)
   uint64_t chunk_bytes;     // head-region chunk size C0 (a multiple of the stage size)
   uint64_t tail_chunk_bytes;// tail-region chunk size C1 (smaller: short tail imbalance)

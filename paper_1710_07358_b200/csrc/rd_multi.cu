@@ -61,11 +61,12 @@ rd_status rd_comm_init(rd_comm_t* comm, int nranks, int rank, const rd_unique_id
   void* p = nullptr;
   e = cudaMalloc(&p, sizeof(rd_record) * (nranks + 1) + 64);
   if (e != cudaSuccess) { ncclCommDestroy(c->nccl); delete c; return rd::cuda_fail(e, "cudaMalloc"); }
-  cudaMemset(p, 0, sizeof(rd_record) * (nranks + 1) + 64);
+  e = cudaMemset(p, 0, sizeof(rd_record) * (nranks + 1) + 64);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { cudaFree(p); ncclCommDestroy(c->nccl); delete c; return rd::cuda_fail(e, "comm buffers"); }
   c->d_send = (rd_record*)p;
   c->d_recv = c->d_send + 1;
   c->d_err = (int*)(c->d_recv + nranks);
-  cudaDeviceSynchronize();
   *comm = c;
   return RD_OK;
 }
