@@ -31,6 +31,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: NCCL's own messages (e.g. the version
+# banner some environments enable with NCCL_DEBUG=VERSION) go to stderr
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "reduce GB/s and % of HBM peak (fp32/int32, n=2^28..2^34) at 1/2/4/8 B200"
 NP_BYTES = {"int32": 4, "uint32": 4, "int64": 8, "float32": 4, "float64": 8}
