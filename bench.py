@@ -31,9 +31,15 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: NCCL's own messages (e.g. the version
-# banner some environments enable with NCCL_DEBUG=VERSION) go to stderr
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+# stdout carries exactly one JSON line. Everything else written to fd 1 --
+# library banners such as NCCL's "NCCL version ..." -- is sent to stderr:
+# fd 1 is re-pointed at stderr and the JSON line goes to a dup of the real one.
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    print(json.dumps(line), file=_JSON_OUT, flush=True)
 
 METRIC = "reduce GB/s and % of HBM peak (fp32/int32, n=2^28..2^34) at 1/2/4/8 B200"
 NP_BYTES = {"int32": 4, "uint32": 4, "int64": 8, "float32": 4, "float64": 8}
@@ -159,7 +165,7 @@ def run_reference(args):
                          "sample": f"first {m} of {n_full} elements per step, {args.steps} steps"},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -390,7 +396,7 @@ def run_b200(args):
             "clocks": clocks,
             "context": {"torch_sum_gbs": tctx, "result": res},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if use_comm:
         import torch.distributed as dist
         dist.barrier()
