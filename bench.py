@@ -201,23 +201,28 @@ def run_b200(args):
     if use_comm and args.exchange == "fused":
         # the exchange fused into the reduce kernel, verified against
         # the NCCL path on this data before it is timed: both fold the same W
-        # records in rank order, so the bits must agree on every rank
+        # records in rank order, so the bits must agree on every rank. Every
+        # step below is collective-safe: a failure on one rank makes all ranks
+        # fall back to NCCL together (a stuck peer surfaces as RD_ERR_TIMEOUT).
         import torch.distributed as dist
-        ok = torch.zeros(1, device=dev)
-        fused = None
+        fused, a_f = None, None
+        ok = torch.ones(1, device=dev)
         try:
-            fused = rd.FusedComm.from_process_group()
+            fused = rd.FusedComm.from_process_group()       # raises on all ranks or none
             a_f = fused.reduce(x, op)
-            a_n = comm.reduce(x, op)
             fused.check()
+        except Exception as e:
+            print(f"[bench] fused exchange unavailable on rank {rank}: {e}", file=sys.stderr)
+            ok.fill_(0.0)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if ok.item() == 1.0:
+            a_n = comm.reduce(x, op)
             comm.check()
             pairs = zip(a_f, a_n) if op in rd.ARG_OPS else [(a_f, a_n)]
             same = all(bool((u.reshape(1).view(torch.uint8) == v.reshape(1).view(torch.uint8)).all().item())
                        for u, v in pairs)
             ok.fill_(1.0 if same else 0.0)
-        except Exception as e:  # IPC unavailable, timeout, mismatch: keep NCCL
-            print(f"[bench] fused exchange unavailable on rank {rank}: {e}", file=sys.stderr)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if ok.item() == 1.0:
             comm.destroy()
             comm, exchange = fused, "fused"

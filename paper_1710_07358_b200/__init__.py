@@ -295,16 +295,34 @@ class FusedComm:
 
     @classmethod
     def from_process_group(cls, group=None, device: int | None = None) -> "FusedComm":
-        """One process per GPU: exchange the mailboxes' IPC handles over the group."""
+        """One process per GPU: exchange the mailboxes' IPC handles over the group.
+        Collective: it either succeeds on every rank or raises on every rank
+        (a rank that cannot create or map a mailbox never leaves its peers
+        waiting in a later exchange)."""
         torch = _torch()
         import torch.distributed as dist
         rank, nranks = dist.get_rank(group), dist.get_world_size(group)
         dev = torch.cuda.current_device() if device is None else device
-        comm, mine = cls._create(nranks, rank, dev, True)
+        comm, mine, err = None, None, None
+        try:
+            comm, mine = cls._create(nranks, rank, dev, True)
+        except ReduceError as e:
+            err = e
         handles = [None] * nranks
         dist.all_gather_object(handles, mine, group=group)
-        blob = b"".join(handles)
-        check(lib().rd_fused_connect(comm.handle, blob), "rd_fused_connect")
+        ok = err is None and all(h is not None for h in handles)
+        if ok:
+            try:
+                check(lib().rd_fused_connect(comm.handle, b"".join(handles)), "rd_fused_connect")
+            except ReduceError as e:
+                err, ok = e, False
+        flags = [None] * nranks
+        dist.all_gather_object(flags, ok, group=group)
+        if not all(flags):
+            if comm is not None:
+                comm.destroy()
+            raise ReduceError(int(err.status) if err is not None else 4,
+                              f"FusedComm.from_process_group (rank {rank}: {err}; ranks ok: {flags})")
         return comm
 
     @classmethod

@@ -74,6 +74,13 @@ def _worker(rank, world, port, outdir):
             acc.merge(g)
         except oracle.OracleError:
             mismatch = True
+    # FusedComm.from_process_group is collective-safe: with no GPU here mailbox
+    # creation fails, and every rank raises (none is left waiting in an exchange)
+    fused_raised = False
+    try:
+        rd.FusedComm.from_process_group(device=0)
+    except rd.ReduceError:
+        fused_raised = True
     # NCCL unique id broadcast (what Comm.from_process_group does before rd_comm_init)
     uid = rd.broadcast_unique_id()
     uid_bytes = ctypes.string_at(ctypes.addressof(uid), 128)
@@ -81,7 +88,7 @@ def _worker(rank, world, port, outdir):
     dist.all_gather_object(ids, uid_bytes)
     import pickle
     with open(os.path.join(outdir, f"rank{rank}.pkl"), "wb") as fh:
-        pickle.dump({"results": results, "mismatch": mismatch, "ids": ids}, fh)
+        pickle.dump({"results": results, "mismatch": mismatch, "ids": ids, "fused_raised": fused_raised}, fh)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -111,5 +118,6 @@ def test_two_rank_shard_exchange_and_rank_order_fold():
         else:
             assert vbytes == full.value.tobytes(), (n, dtype, op)
     assert outs[0]["mismatch"] and outs[1]["mismatch"]
+    assert outs[0]["fused_raised"] and outs[1]["fused_raised"]
     assert outs[0]["ids"][0] == outs[0]["ids"][1] == outs[1]["ids"][0]
     assert outs[0]["ids"][0] != bytes(128)
