@@ -14,6 +14,7 @@ float64; semantics and tolerances are stated in include/b200reduce.h.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 
 import numpy as np
@@ -105,6 +106,15 @@ def _result(out, dtype, op):
     return _arg_view(out, dtype) if op in ARG_OPS else out
 
 
+def _dev_guard(t):
+    """The C library launches on the CURRENT device: make it t's device."""
+    torch = _torch()
+    idx = t.device.index
+    if idx is None or idx == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(idx)
+
+
 def _check_input(x):
     if not x.is_cuda:
         raise ValueError("x must be a CUDA tensor (use reduce_host for host arrays)")
@@ -118,8 +128,9 @@ def reduce(x, op: str, out=None, stream=None):
     tensors (views of one 16-byte rd_arg_result; `out` is then 2 x int64)."""
     _check_input(x)
     out = _new_out(x.dtype, x.device, op) if out is None else _check_out(out, x.dtype, op)
-    check(lib().reduce(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
-                       out.data_ptr(), _stream(x, stream)), "reduce")
+    with _dev_guard(x):
+        check(lib().reduce(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
+                           out.data_ptr(), _stream(x, stream)), "reduce")
     return _result(out, x.dtype, op)
 
 
@@ -129,8 +140,9 @@ def reduce_partial(x, op: str, rec=None, stream=None):
     _check_input(x)
     if rec is None:
         rec = torch.empty(RECORD_BYTES, dtype=torch.uint8, device=x.device)
-    check(lib().reduce_partial(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
-                               rec.data_ptr(), _stream(x, stream)), "reduce_partial")
+    with _dev_guard(x):
+        check(lib().reduce_partial(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
+                                   rec.data_ptr(), _stream(x, stream)), "reduce_partial")
     return rec
 
 
@@ -145,12 +157,13 @@ def combine_records(recs, dtype, op: str, out=None, rec_out=None, status=None, s
         out = _new_out(tdt, recs.device, op)
     elif out is not None:
         _check_out(out, tdt, op)
-    check(lib().rd_combine_records(recs.data_ptr() if recs.numel() else None, recs.numel() // RECORD_BYTES,
-                                   DTYPE_NAMES[name], _op(op),
-                                   out.data_ptr() if out is not None else None,
-                                   rec_out.data_ptr() if rec_out is not None else None,
-                                   status.data_ptr() if status is not None else None,
-                                   _stream(recs, stream)), "rd_combine_records")
+    with _dev_guard(recs):
+        check(lib().rd_combine_records(recs.data_ptr() if recs.numel() else None, recs.numel() // RECORD_BYTES,
+                                       DTYPE_NAMES[name], _op(op),
+                                       out.data_ptr() if out is not None else None,
+                                       rec_out.data_ptr() if rec_out is not None else None,
+                                       status.data_ptr() if status is not None else None,
+                                       _stream(recs, stream)), "rd_combine_records")
     return _result(out, tdt, op) if out is not None else rec_out
 
 
@@ -186,9 +199,10 @@ def reduce_ex(x, op: str, variant: str = "auto", unroll: int = 0, vec_bytes: int
     out = _new_out(x.dtype, x.device, op) if out is None else _check_out(out, x.dtype, op)
     cfg = _lib.rd_config(VARIANTS[variant], vec_bytes, unroll, 0, grid)
     info = _lib.rd_launch_info()
-    check(lib().rd_reduce_ex(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
-                             out.data_ptr(), _stream(x, stream), ctypes.byref(cfg), ctypes.byref(info)),
-          "rd_reduce_ex")
+    with _dev_guard(x):
+        check(lib().rd_reduce_ex(x.data_ptr() if x.numel() else None, x.numel(), _dt(x), _op(op),
+                                 out.data_ptr(), _stream(x, stream), ctypes.byref(cfg), ctypes.byref(info)),
+              "rd_reduce_ex")
     d = {k: getattr(info, k) for k, _ in _lib.rd_launch_info._fields_ if k != "reserved"}
     d["variant"] = {v: k for k, v in VARIANTS.items()}[d["variant"]]
     return _result(out, x.dtype, op), d
@@ -272,9 +286,10 @@ def reduce_multi(x_local, op: str, comm: Comm, out=None, stream=None):
     every rank receives the bitwise-identical result."""
     _check_input(x_local)
     out = _new_out(x_local.dtype, x_local.device, op) if out is None else _check_out(out, x_local.dtype, op)
-    check(lib().reduce_multi(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
-                             _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
-                             comm.handle), "reduce_multi")
+    with _dev_guard(x_local):
+        check(lib().reduce_multi(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
+                                 _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
+                                 comm.handle), "reduce_multi")
     return _result(out, x_local.dtype, op)
 
 
@@ -342,9 +357,10 @@ class FusedComm:
     def reduce(self, x_local, op: str, out=None, stream=None):
         _check_input(x_local)
         out = _new_out(x_local.dtype, x_local.device, op) if out is None else _check_out(out, x_local.dtype, op)
-        check(lib().reduce_fused(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
-                                 _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
-                                 self.handle), "reduce_fused")
+        with _dev_guard(x_local):
+            check(lib().reduce_fused(x_local.data_ptr() if x_local.numel() else None, x_local.numel(),
+                                     _dt(x_local), _op(op), out.data_ptr(), _stream(x_local, stream),
+                                     self.handle), "reduce_fused")
         return _result(out, x_local.dtype, op)
 
     def check(self, stream=None):
