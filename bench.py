@@ -380,7 +380,7 @@ def run_b200(args):
 
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": ws, "steps": K,
-            "warmup": args.warmup, "ms_per_step": round(total_ms / K, 5), "higher_is_better": True,
+            "warmup": max(3, args.warmup), "ms_per_step": round(total_ms / K, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_TAG[dt], "data": "synthetic",
             "config": {"workload": f"{dt} {op}, n=2^{args.log2n} per GPU ({wl}, seed 1), BASELINE configs[1]",
                        "n_per_gpu": n, "n_total": n * ws, "op": op,
