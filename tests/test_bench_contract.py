@@ -45,3 +45,13 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert "workload" in d["config"]
+
+
+def test_table3_percentage_reading():
+    """Reading R12: the printed 99.4 is 100*T_k7/T_new, not the
+    100*T_new/T_k7 the text states, which would give 100.57."""
+    with open(os.path.join(ROOT, "tests", "golden", "table3.txt")) as f:
+        row = [l for l in f if l.strip() and not l.startswith("#")][0]
+    t_k7, t_new, printed = (float(c) for c in row.split("|"))
+    assert round(100 * t_k7 / t_new, 1) == printed
+    assert round(100 * t_new / t_k7, 1) != printed
