@@ -27,7 +27,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 # restated codes (not imported from the CUDA package)
 DTYPES = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
 OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "and": 4, "or": 5, "xor": 6, "argmin": 7, "argmax": 8,
-       "sum_compensated": 9}
+       "sum_compensated": 9, "sum_exact": 10}
 NP_DTYPES = {"int32": np.int32, "uint32": np.uint32, "int64": np.int64,
              "float32": np.float32, "float64": np.float64}
 
@@ -38,7 +38,10 @@ class OracleState(ctypes.Structure):
                 ("hi", ctypes.c_double), ("lo", ctypes.c_double),
                 ("abs_hi", ctypes.c_double), ("abs_lo", ctypes.c_double),
                 ("all_negzero", ctypes.c_int32), ("pad", ctypes.c_int32),
-                ("best_idx", ctypes.c_uint64)]
+                ("best_idx", ctypes.c_uint64),
+                ("big", ctypes.c_uint32 * 72),
+                ("nan_seen", ctypes.c_int32), ("pinf_seen", ctypes.c_int32),
+                ("ninf_seen", ctypes.c_int32), ("pad2", ctypes.c_int32)]
 
 
 def build(force: bool = False) -> str:

@@ -32,6 +32,15 @@
  *      min / max under R4's order together with the SMALLEST index attaining
  *      it; a NaN anywhere wins (value NaN, index of the first NaN); -0.0 ranks
  *      below +0.0; empty input -> identity value and index -1.
+ *  R17 The exact sum ("reproducible": P:50 fn 2 shows
+ *      that float + depends on the evaluation order, fn 3 names the
+ *      mitigations): the real-number sum of the n float values, computed
+ *      exactly, rounded ONCE to the dtype (round to nearest, ties to even).
+ *      It is the one float result no evaluation order can change. Specials:
+ *      any NaN, or +inf together with -inf -> NaN; else any +-inf -> that inf;
+ *      a finite exact sum beyond the dtype's range rounds to +-inf; an exact
+ *      zero is -0.0 iff every term is -0.0 (R2), else +0.0; n == 0 -> +0.0.
+ *      Integers: identical to the sum (already exact).
  *
  * Parity pins for every function: tests/test_oracle_pins.py (DESIGN.md
  * "Oracle pins"). No function here is "parity unpinned".
@@ -43,8 +52,15 @@
 /* dtype / op / status numbers (restated, see header comment) */
 enum { OR_INT32 = 0, OR_UINT32 = 1, OR_INT64 = 2, OR_FLOAT32 = 3, OR_FLOAT64 = 4 };
 enum { OR_SUM = 0, OR_PROD = 1, OR_MIN = 2, OR_MAX = 3, OR_AND = 4, OR_OR = 5, OR_XOR = 6,
-       OR_ARGMIN = 7, OR_ARGMAX = 8, OR_SUM_COMPENSATED = 9 };
+       OR_ARGMIN = 7, OR_ARGMAX = 8, OR_SUM_COMPENSATED = 9, OR_SUM_EXACT = 10 };
 enum { OR_OK = 0, OR_INVALID = 1, OR_UNSUPPORTED = 2 };
+
+/* R17: the exact sum is a two's-complement fixed-point integer of
+ * OR_BIG_LIMBS 32-bit limbs whose unit (bit 0) is the dtype's smallest
+ * subnormal, 2^-149 (fp32) / 2^-1074 (fp64): every finite value of the dtype
+ * is an integer multiple of it, below 2^(128+149) / 2^(1024+1074), so 2304
+ * bits hold any sum of < 2^40 terms with room to spare. */
+#define OR_BIG_LIMBS 72
 
 /* Fold state; mirrored by oracle/__init__.py (ctypes). */
 typedef struct {
@@ -56,6 +72,8 @@ typedef struct {
   int32_t all_negzero;  /* every float term so far is -0.0 (reading R2)     */
   int32_t pad;
   uint64_t best_idx;    /* argmin / argmax: index of the current best (R6)  */
+  uint32_t big[OR_BIG_LIMBS]; /* exact sum (R17), little-endian limbs       */
+  int32_t nan_seen, pinf_seen, ninf_seen, pad2;   /* exact sum: specials    */
 } or_state;
 
 static int is_float(int dt) { return dt == OR_FLOAT32 || dt == OR_FLOAT64; }
@@ -109,12 +127,89 @@ static double ieee_max(double a, double b) {
 
 static int is_arg(int op) { return op == OR_ARGMIN || op == OR_ARGMAX; }
 
+/* ---- exact sum (R17): plain multi-limb integer arithmetic ------------------ */
+static int lsb_exp(int dt) { return dt == OR_FLOAT32 ? -149 : -1074; }
+
+/* big += v * 2^(32k) (v < 2^96 given as three limbs), mod 2^(32*OR_BIG_LIMBS) */
+static void big_add3(uint32_t* big, int k, const uint32_t v[3]) {
+  uint64_t carry = 0;
+  for (int i = k; i < OR_BIG_LIMBS; ++i) {
+    uint64_t t = (uint64_t)big[i] + carry + (i - k < 3 ? v[i - k] : 0);
+    big[i] = (uint32_t)t;
+    carry = t >> 32;
+    if (i - k >= 2 && carry == 0) break;
+  }
+}
+/* big -= v * 2^(32k) */
+static void big_sub3(uint32_t* big, int k, const uint32_t v[3]) {
+  uint64_t borrow = 0;
+  for (int i = k; i < OR_BIG_LIMBS; ++i) {
+    uint64_t sub = (uint64_t)(i - k < 3 ? v[i - k] : 0) + borrow;
+    borrow = (uint64_t)big[i] < sub;
+    big[i] = (uint32_t)((uint64_t)big[i] - sub);
+    if (i - k >= 2 && borrow == 0) break;
+  }
+}
+/* big += x exactly, x finite (x is an integer multiple of 2^lsb) */
+static void big_add_float(uint32_t* big, double x, int lsb) {
+  if (x == 0.0) return;
+  int e;
+  double m = frexp(fabs(x), &e);            /* |x| = m * 2^e, 0.5 <= m < 1 */
+  uint64_t M = (uint64_t)ldexp(m, 53);      /* |x| = M * 2^(e-53), exact */
+  int pos = e - 53 - lsb;                   /* bit position of M's unit */
+  while (pos < 0) { M >>= 1; ++pos; }       /* drops only zero bits (x is a multiple of 2^lsb) */
+  unsigned __int128 v = (unsigned __int128)M << (pos % 32);
+  const uint32_t limbs[3] = {(uint32_t)v, (uint32_t)(v >> 32), (uint32_t)(v >> 64)};
+  if (x > 0) big_add3(big, pos / 32, limbs);
+  else big_sub3(big, pos / 32, limbs);
+}
+static int big_bit(const uint32_t* b, int i) { return i < 0 ? 0 : (int)((b[i / 32] >> (i % 32)) & 1u); }
+
+/* The fixed-point integer `big` times 2^lsb, rounded to p significant bits
+ * (round to nearest, ties to even); returned as a double (exact for p <= 53,
+ * +-inf past the double range). */
+static double big_round(const uint32_t* big_in, int p, int lsb) {
+  uint32_t b[OR_BIG_LIMBS];
+  memcpy(b, big_in, sizeof(b));
+  const int neg = (int)(b[OR_BIG_LIMBS - 1] >> 31);
+  if (neg) {                                 /* magnitude: two's complement negation */
+    uint64_t carry = 1;
+    for (int i = 0; i < OR_BIG_LIMBS; ++i) {
+      uint64_t t = (uint64_t)(uint32_t)~b[i] + carry;
+      b[i] = (uint32_t)t;
+      carry = t >> 32;
+    }
+  }
+  int P = -1;                                /* highest set bit */
+  for (int i = 32 * OR_BIG_LIMBS - 1; i >= 0; --i)
+    if (big_bit(b, i)) { P = i; break; }
+  if (P < 0) return 0.0;
+  double mag;
+  if (P < p) {                               /* fits: exact */
+    uint64_t q = 0;
+    for (int i = P; i >= 0; --i) q = 2 * q + (uint64_t)big_bit(b, i);
+    mag = ldexp((double)q, lsb);
+  } else {
+    const int shift = P + 1 - p;             /* bits below the p kept ones */
+    uint64_t q = 0;
+    for (int i = P; i >= shift; --i) q = 2 * q + (uint64_t)big_bit(b, i);
+    const int half = big_bit(b, shift - 1);
+    int sticky = 0;
+    for (int i = shift - 2; i >= 0 && !sticky; --i) sticky = big_bit(b, i);
+    if (half && (sticky || (q & 1u))) q += 1; /* ties to even */
+    mag = ldexp((double)q, shift + lsb);     /* q <= 2^p: exact, or inf */
+  }
+  return neg ? -mag : mag;
+}
+
 int or_init(or_state* st, int dtype, int op) {
-  if (!st || dtype < 0 || dtype > 4 || op < 0 || op > 9) return OR_INVALID;
+  if (!st || dtype < 0 || dtype > 4 || op < 0 || op > 10) return OR_INVALID;
+  /* integer sums are exact already (R17) */
+  if (op == OR_SUM_EXACT && !is_float(dtype)) op = OR_SUM;
   /* the compensated sum of the library has the same definition as
    * the sum; this oracle's sum accumulators are already fp64 / double-double */
   if (op == OR_SUM_COMPENSATED) op = OR_SUM;
-  if (is_float(dtype) && op >= OR_AND && !is_arg(op)) return OR_UNSUPPORTED; /* R5 */
+  if (is_float(dtype) && op >= OR_AND && op <= OR_XOR) return OR_UNSUPPORTED; /* R5 */
   memset(st, 0, sizeof(*st));
   st->dtype = dtype;
   st->op = op;
@@ -200,6 +295,13 @@ static void fold_one(or_state* st, const unsigned char* p) {
   else memcpy(&x, p, 8);
   dd_add(&st->abs_hi, &st->abs_lo, fabs(x));
   if (!(x == 0.0 && signbit(x))) st->all_negzero = 0;
+  if (op == OR_SUM_EXACT) {       /* R17: the fold adds x_i to the exact sum */
+    if (isnan(x)) st->nan_seen = 1;
+    else if (isinf(x)) { if (x > 0) st->pinf_seen = 1; else st->ninf_seen = 1; }
+    else big_add_float(st->big, x, lsb_exp(dt));
+    st->count++;
+    return;
+  }
   if (st->count == 0) {           /* R2: the fold starts at x_0 */
     st->hi = x; st->lo = 0.0; st->count = 1;
     return;
@@ -232,8 +334,8 @@ int or_fold(or_state* st, const void* x, uint64_t n) {
 /* Result of an empty fold: Algorithm 1's initial accumulator (R1); argmin /
  * argmax report the min / max identity value (their index is -1). */
 int or_identity(int dtype, int op, void* out) {
-  if (!out || dtype < 0 || dtype > 4 || op < 0 || op > 9) return OR_INVALID;
-  if (op == OR_SUM_COMPENSATED) op = OR_SUM;
+  if (!out || dtype < 0 || dtype > 4 || op < 0 || op > 10) return OR_INVALID;
+  if (op == OR_SUM_COMPENSATED || op == OR_SUM_EXACT) op = OR_SUM;
   if (op == OR_ARGMIN) op = OR_MIN;
   if (op == OR_ARGMAX) op = OR_MAX;
   if (is_float(dtype) && op >= OR_AND) return OR_UNSUPPORTED;
@@ -286,6 +388,22 @@ int or_result(const or_state* st, void* value_out, double* hi, double* lo, doubl
     if (sum_abs) *sum_abs = 0.0;
     return OR_OK;
   }
+  if (st->op == OR_SUM_EXACT) {   /* R17: one rounding of the exact sum */
+    double v;
+    if (st->nan_seen || (st->pinf_seen && st->ninf_seen)) v = NAN;
+    else if (st->pinf_seen) v = INFINITY;
+    else if (st->ninf_seen) v = -INFINITY;
+    else {
+      v = big_round(st->big, st->dtype == OR_FLOAT32 ? 24 : 53, lsb_exp(st->dtype));
+      if (v == 0.0) v = st->all_negzero ? -0.0 : 0.0;
+    }
+    if (st->dtype == OR_FLOAT32) { float f = (float)v; memcpy(value_out, &f, 4); } /* exact or inf */
+    else memcpy(value_out, &v, 8);
+    if (hi) *hi = v;
+    if (lo) *lo = 0.0;
+    if (sum_abs) *sum_abs = st->abs_hi + st->abs_lo;
+    return OR_OK;
+  }
   double v = (st->lo == 0.0) ? st->hi : st->hi + st->lo; /* double-double -> double; keeps -0.0 */
   if (!isfinite(st->hi)) v = st->hi;
   if (v == 0.0 && (st->op == OR_SUM)) v = st->all_negzero ? -0.0 : 0.0; /* R2 */
@@ -331,6 +449,19 @@ int or_merge(or_state* a, const or_state* b) {
   }
   if (!is_float(dt)) {
     a->ibits = int_combine(dt, op, a->ibits, b->ibits);
+  } else if (op == OR_SUM_EXACT) {  /* exact sums add exactly */
+    uint64_t carry = 0;
+    for (int i = 0; i < OR_BIG_LIMBS; ++i) {
+      uint64_t t = (uint64_t)a->big[i] + b->big[i] + carry;
+      a->big[i] = (uint32_t)t;
+      carry = t >> 32;
+    }
+    a->nan_seen |= b->nan_seen;
+    a->pinf_seen |= b->pinf_seen;
+    a->ninf_seen |= b->ninf_seen;
+    dd_add(&a->abs_hi, &a->abs_lo, b->abs_hi);
+    dd_add(&a->abs_hi, &a->abs_lo, b->abs_lo);
+    a->all_negzero = a->all_negzero && b->all_negzero;
   } else {
     switch (op) {
       case OR_SUM:
