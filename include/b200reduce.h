@@ -76,7 +76,19 @@ typedef enum {
    * |result - exact| <= 0.5 ulp(result) + 4 * u_acc * sum|x_i| on the
    * workloads of DESIGN.md, u_acc = 2^-53 (fp32 data) / 2^-106 (fp64 data).
    * Integers: identical to RD_SUM. */
-  RD_SUM_COMPENSATED = 9
+  RD_SUM_COMPENSATED = 9,
+  /* SURVEY §8(f) f2, reproducible: the EXACT sum rounded once (round to
+   * nearest, ties to even) -- DESIGN.md reading R17. P:50 fn 2: the real sum
+   * "is always the same, no matter the order the terms are added"; this is
+   * that sum, so the bits do not depend on the grid, variant, base alignment
+   * or number of GPUs. Any NaN, or +inf with -inf -> NaN; else +-inf if any;
+   * a finite exact sum past the dtype's range -> +-inf; an exact zero is -0.0
+   * iff every term is -0.0. Floats: reduce, reduce_multi, reduce_host and
+   * reduce_exact_partial / rd_combine_exact_records (the 32-byte rd_record
+   * cannot carry an exact partial, so reduce_partial, rd_combine_records and
+   * reduce_fused return RD_ERR_UNSUPPORTED for float dtypes).
+   * Integers: identical to RD_SUM everywhere. */
+  RD_SUM_EXACT = 10
 } rd_op;
 
 /* Output of RD_ARGMIN / RD_ARGMAX (16 bytes, 8-byte aligned). */
@@ -119,6 +131,27 @@ typedef struct rd_record {
   uint64_t acc[2];
 } rd_record;
 
+/*
+ * rd_exact_record -- the exact partial sum of one block of float X
+ * (RD_SUM_EXACT): a fixed-point integer sum_k word[k] * 2^(32k) in units of
+ * the dtype's smallest subnormal (2^-149 for float32, 2^-1074 for float64),
+ * words carried to digits in [0, 2^32) except the signed top word
+ * word[nwords-1]; nwords = 12 (float32) / 68 (float64), the rest zero.
+ *   flags = 1 NaN seen | 2 +inf seen | 4 -inf seen | 8 some term is not -0.0
+ * 608 bytes, plain data, 16-byte aligned when allocated so. Adding the words
+ * of two records is the exact sum of the two blocks (any order).
+ */
+#define RD_EXACT_MAX_WORDS 72
+typedef struct rd_exact_record {
+  uint32_t tag;
+  uint32_t status;
+  uint64_t n;
+  uint32_t flags;
+  uint32_t nwords;
+  uint64_t reserved;
+  int64_t word[RD_EXACT_MAX_WORDS];
+} rd_exact_record;
+
 /* ------------------------------------------------------------------ reduce
  * reduce -- out[0] = x_0 (x) ... (x) x_{n-1} on one GPU.
  *   x      device pointer to n contiguous elements of `dtype` (caller-owned,
@@ -149,6 +182,22 @@ rd_status reduce_partial(const void* x, size_t n, rd_dtype dtype, rd_op op, rd_r
  * NULL), MISALIGNED (recs not 16-byte aligned), UNSUPPORTED, CUDA. */
 rd_status rd_combine_records(const rd_record* recs, int count, rd_dtype dtype, rd_op op,
                              void* out, rd_record* rec_out, int* d_status, rd_stream_t stream);
+
+/* reduce_exact_partial -- the exact partial of float x[0..n) (RD_SUM_EXACT)
+ * as one rd_exact_record at device pointer `rec` (8-byte aligned).
+ * Errors: as reduce_partial; UNSUPPORTED for integer dtypes (use
+ * reduce_partial with RD_SUM, which is exact). */
+rd_status reduce_exact_partial(const void* x, size_t n, rd_dtype dtype, rd_exact_record* rec,
+                               rd_stream_t stream);
+
+/* rd_combine_exact_records -- add `count` device exact records (float
+ * dtype) and write the once-rounded value to device `out` (may be NULL)
+ * and/or the summed record to device `rec_out` (may be NULL). A record whose
+ * tag or nwords differs sets *d_status (device int, may be NULL) to
+ * RD_ERR_MISMATCH and `out` receives +0.0. One CTA. Errors: INVALID_ARG,
+ * MISALIGNED (recs not 16-byte aligned), UNSUPPORTED (integer dtype), CUDA. */
+rd_status rd_combine_exact_records(const rd_exact_record* recs, int count, rd_dtype dtype, void* out,
+                                   rd_exact_record* rec_out, int* d_status, rd_stream_t stream);
 
 /* reduce_host -- end-to-end reduction of a HOST array (pinned or pageable)
  * on the current device: chunks are copied host->device on a copy stream,

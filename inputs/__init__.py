@@ -25,7 +25,7 @@ NP_DTYPES = {"int32": np.int32, "uint32": np.uint32, "int64": np.int64,
              "float32": np.float32, "float64": np.float64}
 WORKLOADS = {"iota": 0, "uniform_bits": 1, "odd": 2, "sparse_clear": 3, "sparse_set": 4,
              "u01": 5, "normalish": 6, "near_one": 7, "pow2_sparse": 8, "planted": 9,
-             "int_small": 10, "sparse_pm1": 11}
+             "int_small": 10, "sparse_pm1": 11, "wide": 12, "wide_full": 13}
 
 # Workload used for each op on each dtype class: non-degenerate
 # for products (odd / near-one) and for and/or (sparse bit patterns).
@@ -39,6 +39,8 @@ DEFAULT_WORKLOAD = {
     ("int", "argmin"): "int_small", ("int", "argmax"): "int_small",
     ("float", "argmin"): "u01", ("float", "argmax"): "u01",
     ("int", "sum_compensated"): "uniform_bits", ("float", "sum_compensated"): "normalish",
+    # exact sum: terms spanning 2^-40..2^40 (most additions inexact: the slow path works)
+    ("int", "sum_exact"): "uniform_bits", ("float", "sum_exact"): "wide",
 }
 
 

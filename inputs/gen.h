@@ -43,7 +43,10 @@ enum {
   GEN_PLANTED = 9,         /* one planted max and one planted min              */
   GEN_INT_SMALL = 10,      /* integers in [-65536, 65536] (exact in fp64 sums) */
   GEN_SPARSE_PM1 = 11,     /* 0, or +-1 at <= ~2^20 hashed positions           */
-  GEN_NUM_WORKLOADS = 12
+  GEN_WIDE = 12,           /* floats: random sign, mantissa, exponent in [-40, 40] */
+  GEN_WIDE_FULL = 13,      /* floats: random sign, mantissa, ANY finite exponent
+                              field (subnormals through the largest binade)    */
+  GEN_NUM_WORKLOADS = 14
 };
 
 #define GEN_GOLDEN 0x9E3779B97F4A7C15ULL
@@ -178,6 +181,18 @@ GEN_HD int gen_element(int dt, int wl, uint64_t seed, uint64_t i, uint64_t n_tot
       int64_t v = 0;
       if ((h >> 32) < gen_threshold(1ULL << 20, n_total)) v = (h & 1ULL) ? 1 : -1;
       ff = (float)v; fd = (double)v; ib = (uint64_t)v;
+      break;
+    }
+    case GEN_WIDE:
+    case GEN_WIDE_FULL: {
+      /* built from bits: sign = bit 63, mantissa = low bits, exponent field
+       * from bits 32.. (wide: 2^-40 .. 2^40; full: 0 .. max finite field) */
+      if (!is_float) return -1;
+      const uint64_t sg = h >> 63;
+      const uint64_t e32 = (wl == GEN_WIDE) ? 127 - 40 + ((h >> 32) % 81ULL) : (h >> 32) % 255ULL;
+      const uint64_t e64 = (wl == GEN_WIDE) ? 1023 - 40 + ((h >> 32) % 81ULL) : (h >> 32) % 2047ULL;
+      ff = gen_bits_to_f32((uint32_t)((sg << 31) | (e32 << 23) | (h & 0x7FFFFFULL)));
+      fd = gen_bits_to_f64((sg << 63) | (e64 << 52) | ((h * GEN_GOLDEN) & 0xFFFFFFFFFFFFFULL));
       break;
     }
     default:

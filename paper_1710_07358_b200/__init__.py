@@ -22,17 +22,20 @@ import numpy as np
 from . import _lib
 from ._lib import ReduceError, check, lib
 
-__all__ = ["reduce", "reduce_partial", "combine_records", "reduce_host", "reduce_ex",
+__all__ = ["reduce", "reduce_partial", "combine_records", "reduce_exact_partial", "combine_exact_records",
+           "reduce_host", "reduce_ex",
            "reduce_multi", "Comm", "FusedComm", "shard_range", "identity", "release_workspaces",
-           "ReduceError", "OPS", "RECORD_BYTES"]
+           "ReduceError", "OPS", "RECORD_BYTES", "EXACT_RECORD_BYTES"]
 
 OPS = {"sum": _lib.RD_SUM, "prod": _lib.RD_PROD, "min": _lib.RD_MIN, "max": _lib.RD_MAX,
        "and": _lib.RD_AND, "or": _lib.RD_OR, "xor": _lib.RD_XOR,
-       "argmin": _lib.RD_ARGMIN, "argmax": _lib.RD_ARGMAX, "sum_compensated": _lib.RD_SUM_COMPENSATED}
+       "argmin": _lib.RD_ARGMIN, "argmax": _lib.RD_ARGMAX, "sum_compensated": _lib.RD_SUM_COMPENSATED,
+       "sum_exact": _lib.RD_SUM_EXACT}
 ARG_OPS = ("argmin", "argmax")
 DTYPE_NAMES = {"int32": _lib.RD_INT32, "uint32": _lib.RD_UINT32, "int64": _lib.RD_INT64,
                "float32": _lib.RD_FLOAT32, "float64": _lib.RD_FLOAT64}
 RECORD_BYTES = 32
+EXACT_RECORD_BYTES = ctypes.sizeof(_lib.rd_exact_record)   # 608
 VARIANTS = {"auto": _lib.RD_VARIANT_AUTO, "vector": _lib.RD_VARIANT_VECTOR, "paper": _lib.RD_VARIANT_PAPER,
             "bulk": _lib.RD_VARIANT_BULK}
 
@@ -165,6 +168,40 @@ def combine_records(recs, dtype, op: str, out=None, rec_out=None, status=None, s
                                        status.data_ptr() if status is not None else None,
                                        _stream(recs, stream)), "rd_combine_records")
     return _result(out, tdt, op) if out is not None else rec_out
+
+
+def reduce_exact_partial(x, rec=None, stream=None):
+    """Exact partial sum of a float CUDA tensor (RD_SUM_EXACT) as one 608-byte
+    rd_exact_record (uint8 CUDA tensor)."""
+    torch = _torch()
+    _check_input(x)
+    if rec is None:
+        rec = torch.empty(EXACT_RECORD_BYTES, dtype=torch.uint8, device=x.device)
+    with _dev_guard(x):
+        check(lib().reduce_exact_partial(x.data_ptr() if x.numel() else None, x.numel(), _dt(x),
+                                         rec.data_ptr(), _stream(x, stream)), "reduce_exact_partial")
+    return rec
+
+
+def combine_exact_records(recs, dtype, out=None, rec_out=None, status=None, stream=None):
+    """Add k exact records (a uint8 CUDA tensor of k*608 bytes) and round once."""
+    torch = _torch()
+    name = _dtype_name(dtype)
+    tdt = getattr(torch, name)
+    if recs.numel() % EXACT_RECORD_BYTES:
+        raise ValueError("recs must hold whole 608-byte exact records")
+    if out is None and rec_out is None:
+        out = torch.empty((), dtype=tdt, device=recs.device)
+    elif out is not None and out.dtype != tdt:
+        raise ValueError(f"out has dtype {out.dtype}, expected {tdt}")
+    with _dev_guard(recs):
+        check(lib().rd_combine_exact_records(recs.data_ptr() if recs.numel() else None,
+                                             recs.numel() // EXACT_RECORD_BYTES, DTYPE_NAMES[name],
+                                             out.data_ptr() if out is not None else None,
+                                             rec_out.data_ptr() if rec_out is not None else None,
+                                             status.data_ptr() if status is not None else None,
+                                             _stream(recs, stream)), "rd_combine_exact_records")
+    return out if out is not None else rec_out
 
 
 def reduce_host(x, op: str):

@@ -14,7 +14,8 @@ LIB_PATH = os.environ.get("RD_LIB_PATH") or os.path.join(_HERE, "libb200reduce.s
 
 RD_INT32, RD_UINT32, RD_INT64, RD_FLOAT32, RD_FLOAT64 = range(5)
 RD_SUM, RD_PROD, RD_MIN, RD_MAX, RD_AND, RD_OR, RD_XOR = range(7)
-RD_ARGMIN, RD_ARGMAX, RD_SUM_COMPENSATED = 7, 8, 9
+RD_ARGMIN, RD_ARGMAX, RD_SUM_COMPENSATED, RD_SUM_EXACT = 7, 8, 9, 10
+RD_EXACT_MAX_WORDS = 72
 RD_OK = 0
 STATUS = {0: "RD_OK", 1: "RD_ERR_INVALID_ARG", 2: "RD_ERR_UNSUPPORTED", 3: "RD_ERR_MISALIGNED",
           4: "RD_ERR_CUDA", 5: "RD_ERR_NCCL", 6: "RD_ERR_MISMATCH", 7: "RD_ERR_TIMEOUT"}
@@ -24,6 +25,12 @@ RD_VARIANT_AUTO, RD_VARIANT_VECTOR, RD_VARIANT_PAPER, RD_VARIANT_BULK = 0, 1, 2,
 class rd_record(ctypes.Structure):
     _fields_ = [("tag", ctypes.c_uint32), ("status", ctypes.c_uint32), ("n", ctypes.c_uint64),
                 ("acc", ctypes.c_uint64 * 2)]
+
+
+class rd_exact_record(ctypes.Structure):
+    _fields_ = [("tag", ctypes.c_uint32), ("status", ctypes.c_uint32), ("n", ctypes.c_uint64),
+                ("flags", ctypes.c_uint32), ("nwords", ctypes.c_uint32), ("reserved", ctypes.c_uint64),
+                ("word", ctypes.c_int64 * RD_EXACT_MAX_WORDS)]
 
 
 class rd_arg_result(ctypes.Structure):
@@ -52,6 +59,8 @@ SIGNATURES = {
     "reduce": (_i, [_vp, _sz, _i, _i, _vp, _vp]),
     "reduce_partial": (_i, [_vp, _sz, _i, _i, _vp, _vp]),
     "rd_combine_records": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "reduce_exact_partial": (_i, [_vp, _sz, _i, _vp, _vp]),
+    "rd_combine_exact_records": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
     "reduce_host": (_i, [_vp, _sz, _i, _i, _vp]),
     "rd_get_unique_id": (_i, [ctypes.POINTER(rd_unique_id)]),
     "rd_comm_init": (_i, [ctypes.POINTER(_vp), _i, _i, ctypes.POINTER(rd_unique_id), _i]),

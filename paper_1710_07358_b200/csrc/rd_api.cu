@@ -11,6 +11,7 @@
 #include <utility>
 
 #include "b200reduce.h"
+#include "rd_exact.cuh"
 #include "rd_internal.h"
 #include "rd_registry.h"
 
@@ -31,11 +32,15 @@ int dtype_size(int dtype) {
 
 bool is_arg_op(int op) { return op == RD_ARGMIN || op == RD_ARGMAX; }
 
+bool is_exact_float(int dtype, int op) {
+  return op == RD_SUM_EXACT && (dtype == RD_FLOAT32 || dtype == RD_FLOAT64);
+}
+
 int out_size(int dtype, int op) { return is_arg_op(op) ? (int)sizeof(rd_arg_result) : dtype_size(dtype); }
 
 rd_status check_dtype_op(int dtype, int op) {
   if (dtype < RD_INT32 || dtype > RD_FLOAT64) { set_error("unknown dtype"); return RD_ERR_INVALID_ARG; }
-  if (op < RD_SUM || op > RD_SUM_COMPENSATED) { set_error("unknown op"); return RD_ERR_INVALID_ARG; }
+  if (op < RD_SUM || op > RD_SUM_EXACT) { set_error("unknown op"); return RD_ERR_INVALID_ARG; }
   if ((dtype == RD_FLOAT32 || dtype == RD_FLOAT64) && op >= RD_AND && op <= RD_XOR) {
     set_error("bitwise op on a float dtype");
     return RD_ERR_UNSUPPORTED;
@@ -46,8 +51,12 @@ rd_status check_dtype_op(int dtype, int op) {
 // ------------------------------------------------------------------ workspace
 namespace {
 
+// exact-sum CTA slots: kMaxGrid x (kWords + 1) int64 (the largest, fp64)
+constexpr size_t kExactSlotBytes = sizeof(long long) * kMaxGrid * (ExactTraits<double>::kWords + 1);
+
 struct Workspace {
   Slot* partials = nullptr;   // kMaxGrid slots (per CTA, or per chunk for the bulk variant)
+  long long* xpart = nullptr; // exact-sum slots (RD_SUM_EXACT)
   unsigned* ticket = nullptr; // CTAs finished, zero between launches
   unsigned* work = nullptr;   // bulk variant: next chunk, zero between launches
 };
@@ -74,15 +83,17 @@ rd_status get_workspace(int dev, cudaStream_t stream, Workspace* out) {
   }
   Workspace w;
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, sizeof(Slot) * kMaxSlots + 256);
+  const size_t bytes = sizeof(Slot) * kMaxSlots + 256 + kExactSlotBytes;
+  cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) return cuda_fail(e, "workspace cudaMalloc");
   // zeroed in stream order (no device-wide synchronisation: kernels on other
   // streams, e.g. the ranks of a fused exchange, may be running and waiting)
-  e = cudaMemsetAsync(p, 0, sizeof(Slot) * kMaxSlots + 256, stream);
+  e = cudaMemsetAsync(p, 0, bytes, stream);
   if (e != cudaSuccess) { cudaFree(p); return cuda_fail(e, "workspace init"); }
   w.partials = (Slot*)p;
   w.ticket = (unsigned*)((char*)p + sizeof(Slot) * kMaxSlots);
   w.work = w.ticket + 32;     // separate 128-byte line
+  w.xpart = (long long*)((char*)p + sizeof(Slot) * kMaxSlots + 256);
   g_ws[key] = w;
   *out = w;
   return RD_OK;
@@ -149,7 +160,7 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 // communicator is connected.
 rd_status preload_default_kernels(int dev) {
   for (int dt = RD_INT32; dt <= RD_FLOAT64; ++dt) {
-    for (int op = RD_SUM; op <= RD_SUM_COMPENSATED; ++op) {
+    for (int op = RD_SUM; op <= RD_SUM_EXACT; ++op) {
       if (check_dtype_op(dt, op) != RD_OK) continue;
       for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK}) {
         KernelRef k;
@@ -185,6 +196,14 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   if (mode != 1 && (uintptr_t)out % (is_arg_op(op) ? 8 : s) != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
   if (mode == 1 && (uintptr_t)rec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
+  if (is_exact_float(dtype, op)) {
+    if (mode != 0) {
+      set_error("RD_SUM_EXACT on floats: the 32-byte rd_record cannot carry an exact partial "
+                "(use reduce_exact_partial / reduce_multi)");
+      return RD_ERR_UNSUPPORTED;
+    }
+    return launch_exact(x, n, dtype, 0, out, nullptr, stream, cfg, info);
+  }
 
   int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
   const int unroll = cfg ? cfg->unroll : 0;
@@ -325,10 +344,120 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   return RD_OK;
 }
 
+// RD_SUM_EXACT on a float dtype (rd_exact.cuh): validate, plan, launch.
+// mode 0 writes one element to `out`, mode 1 one rd_exact_record to `xrec`.
+rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, rd_exact_record* xrec,
+                       cudaStream_t stream, const rd_config* cfg, rd_launch_info* info) {
+  if (dtype != RD_FLOAT32 && dtype != RD_FLOAT64) {
+    set_error("exact partials are for float dtypes (integer sums are exact: use reduce_partial)");
+    return RD_ERR_UNSUPPORTED;
+  }
+  const int s = dtype_size(dtype);
+  if (x == nullptr && n > 0) { set_error("x is NULL"); return RD_ERR_INVALID_ARG; }
+  if (mode == 0 && out == nullptr) { set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
+  if (mode == 1 && xrec == nullptr) { set_error("rec is NULL"); return RD_ERR_INVALID_ARG; }
+  if ((uintptr_t)x % s != 0) { set_error("x is not aligned to sizeof(dtype)"); return RD_ERR_MISALIGNED; }
+  if (mode == 0 && (uintptr_t)out % s != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
+  if (mode == 1 && (uintptr_t)xrec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
+  if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
+  ExactRef k;
+  if (!lookup_exact(dtype, &k)) { set_error("no compiled exact-sum kernel (RD_TUNE_EXACT?)"); return RD_ERR_UNSUPPORTED; }
+  if (cfg && ((cfg->variant != RD_VARIANT_AUTO && cfg->variant != RD_VARIANT_VECTOR) ||
+              (cfg->unroll && cfg->unroll != k.unroll) || (cfg->vec_bytes && cfg->vec_bytes != k.vec_bytes) ||
+              (cfg->block && cfg->block != k.block))) {
+    set_error("RD_SUM_EXACT has one compiled configuration (vector loads, 32 B, U=6, 256 threads)");
+    return RD_ERR_UNSUPPORTED;
+  }
+  if (cfg && cfg->grid < 0) { set_error("bad rd_config"); return RD_ERR_INVALID_ARG; }
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  rd_status st;
+  DeviceInfo di;
+  if ((st = device_info(dev, &di)) != RD_OK) return st;
+  int occ = 1, regs = 0;
+  KernelRef kr{(ReduceFn)k.fn, k.block, k.unroll, k.vec_bytes, RD_VARIANT_VECTOR};
+  if ((st = occupancy(dev, kr, &occ, &regs)) != RD_OK) return st;
+  Workspace ws;
+  if ((st = get_workspace(dev, stream, &ws)) != RD_OK) return st;
+
+  XArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.x = (const unsigned char*)x;
+  a.n = n;
+  const uint64_t L = (uint64_t)(k.vec_bytes / s);
+  const uint64_t mis = (uint64_t)((uintptr_t)x % (uintptr_t)k.vec_bytes);
+  uint64_t head = ((k.vec_bytes - mis) % k.vec_bytes) / s;
+  if (head > n) head = n;
+  a.head = head;
+  a.nvec = (n - head) / L;
+  a.tail_start = head + a.nvec * L;
+  a.tail = n - a.tail_start;
+  uint64_t g = (uint64_t)di.sms * occ;
+  uint64_t need = (a.nvec + (uint64_t)k.block * k.unroll - 1) / ((uint64_t)k.block * k.unroll);
+  if (need < 1) need = 1;
+  if (g > need) g = need;
+  if (cfg && cfg->grid > 0) g = (uint64_t)cfg->grid;
+  if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
+  a.out = out;
+  a.rec = xrec;
+  a.partials = ws.xpart;
+  a.ticket = ws.ticket;
+  a.tag = record_tag(dtype, RD_SUM_EXACT);
+  a.mode = mode;
+
+  cudaLaunchConfig_t lc;
+  std::memset(&lc, 0, sizeof(lc));
+  lc.gridDim = dim3((unsigned)g);
+  lc.blockDim = dim3((unsigned)k.block);
+  lc.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  e = cudaLaunchKernelEx(&lc, k.fn, a);
+  if (e != cudaSuccess) return cuda_fail(e, "exact-sum kernel launch");
+  if (info) {
+    std::memset(info, 0, sizeof(*info));
+    info->variant = RD_VARIANT_VECTOR;
+    info->vec_bytes = k.vec_bytes;
+    info->unroll = k.unroll;
+    info->block = k.block;
+    info->grid = (int32_t)g;
+    info->regs_per_thread = regs;
+    info->ctas_per_sm = occ;
+    info->head = a.head;
+    info->nvec = a.nvec;
+    info->tail = a.tail;
+  }
+  return RD_OK;
+}
+
+rd_status launch_exact_combine(const rd_exact_record* recs, int count, int dtype, void* out,
+                               rd_exact_record* rec_out, int* d_status, cudaStream_t stream) {
+  if (dtype < RD_INT32 || dtype > RD_FLOAT64) { set_error("unknown dtype"); return RD_ERR_INVALID_ARG; }
+  ExactCombineFn fn = lookup_exact_combine(dtype);
+  if (!fn) { set_error("exact records are for float dtypes"); return RD_ERR_UNSUPPORTED; }
+  if (count < 0 || (count > 0 && recs == nullptr)) { set_error("bad recs/count"); return RD_ERR_INVALID_ARG; }
+  if ((uintptr_t)recs % 16) { set_error("recs must be 16-byte aligned"); return RD_ERR_MISALIGNED; }
+  if (out == nullptr && rec_out == nullptr) { set_error("no output"); return RD_ERR_INVALID_ARG; }
+  if (out && (uintptr_t)out % dtype_size(dtype)) { set_error("out misaligned"); return RD_ERR_MISALIGNED; }
+  if (rec_out && (uintptr_t)rec_out % 8) { set_error("rec_out misaligned"); return RD_ERR_MISALIGNED; }
+  fn<<<1, 128, 0, stream>>>(recs, count, record_tag(dtype, RD_SUM_EXACT), out, rec_out, d_status);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "exact combine kernel launch");
+  return RD_OK;
+}
+
 rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, void* out,
                          rd_record* rec_out, int* d_status, cudaStream_t stream) {
   rd_status st = check_dtype_op(dtype, op);
   if (st != RD_OK) return st;
+  if (is_exact_float(dtype, op)) {
+    set_error("RD_SUM_EXACT on floats: use rd_combine_exact_records (the 32-byte rd_record cannot carry it)");
+    return RD_ERR_UNSUPPORTED;
+  }
   if (count < 0 || (count > 0 && recs == nullptr)) { set_error("bad recs/count"); return RD_ERR_INVALID_ARG; }
   if ((uintptr_t)recs % 16) { set_error("recs must be 16-byte aligned"); return RD_ERR_MISALIGNED; }
   if (out == nullptr && rec_out == nullptr) { set_error("no output"); return RD_ERR_INVALID_ARG; }
@@ -372,6 +501,16 @@ rd_status rd_reduce_ex(const void* x, size_t n, rd_dtype dtype, rd_op op, void* 
   return rd::launch_reduce(x, n, dtype, op, 0, out, nullptr, (cudaStream_t)stream, cfg, info);
 }
 
+rd_status reduce_exact_partial(const void* x, size_t n, rd_dtype dtype, rd_exact_record* rec,
+                               rd_stream_t stream) {
+  return rd::launch_exact(x, n, dtype, 1, nullptr, rec, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+rd_status rd_combine_exact_records(const rd_exact_record* recs, int count, rd_dtype dtype, void* out,
+                                   rd_exact_record* rec_out, int* d_status, rd_stream_t stream) {
+  return rd::launch_exact_combine(recs, count, dtype, out, rec_out, d_status, (cudaStream_t)stream);
+}
+
 rd_status rd_combine_records(const rd_record* recs, int count, rd_dtype dtype, rd_op op, void* out,
                              rd_record* rec_out, int* d_status, rd_stream_t stream) {
   return rd::launch_combine(recs, count, dtype, op, out, rec_out, d_status, (cudaStream_t)stream);
@@ -389,7 +528,7 @@ rd_status rd_identity(rd_dtype dtype, rd_op op, void* host_out) {
     std::memcpy(host_out, &r, sizeof(r));
     return RD_OK;
   }
-  if (op == RD_SUM_COMPENSATED) op = RD_SUM;
+  if (op == RD_SUM_COMPENSATED || op == RD_SUM_EXACT) op = RD_SUM;
   if (dtype == RD_FLOAT32 || dtype == RD_FLOAT64) {
     const double inf = __builtin_huge_val();
     double v = op == RD_SUM ? 0.0 : op == RD_PROD ? 1.0 : op == RD_MIN ? inf : -inf;

@@ -1,0 +1,516 @@
+// rd_exact.cuh -- the exact float sum (RD_SUM_EXACT; SURVEY §8(f) row f2,
+// reading R17): the real sum of the n float values, rounded ONCE to nearest-
+// even. PAPER.md P:50 fn 2 shows that a float sum depends on the order of the
+// additions ("the floating point computed value can result in 0 or 1.5");
+// the exact sum is the one result no order, grid, variant, base alignment or
+// GPU count can change -- so it is bitwise reproducible by construction.
+//
+// Design (one single-pass launch, like rd_vector_kernel):
+//  a1  each thread streams 32-byte vectors grid-stride and adds every element
+//      (fp32 widened to fp64, exactly) into one of E = 4 two-term expansions
+//      (a0, a1) with an error-free TwoSum: a0 + x = s + e exactly. When e == 0
+//      (every term for data whose exponents span < ~29 bits below the running
+//      sum -- the u01 / normal workloads) that is the whole cost: 6 DADD and
+//      one compare per element. A nonzero e goes into a1 by a second TwoSum,
+//      and only a nonzero second error -- or an fp64 overflow, or inf/NaN --
+//      takes the rare slow path into the warp's superaccumulator.
+//  superaccumulator: a fixed-point integer whose unit is the dtype's smallest
+//      subnormal (2^-149 / 2^-1074), held as kWords carry-save int64 words of
+//      32-bit digits in shared memory (one per warp). A finite double is
+//      deposited exactly as three signed digits (shared 64-bit atomics); a word
+//      nearing 2^60 moves its high part to the next word (value-preserving).
+//  a3-a5  at the end every thread deposits its expansions; each warp carries
+//      its words to digits in [0, 2^32); the CTA adds the W warps' digits.
+//  a6  the CTA's words go to workspace slot blockIdx; the last CTA (atomic
+//      ticket) adds the G slots word by word (integers: any order is exact),
+//      carries, and
+//  a7  rounds once: the 64 bits below the leading one give the p kept bits,
+//      the guard bit and (with every lower digit) the sticky bit; ties to even;
+//      the float is assembled as (shift << (p-1)) + q, which carries a rounded-
+//      up mantissa into the exponent and reaches inf exactly at the IEEE
+//      overflow threshold. Specials: flags for NaN, +inf, -inf and "some term
+//      is not -0.0" (reading R2's sign of a zero sum).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "rd_kernels.cuh"
+
+namespace rd {
+
+template <typename T> struct ExactTraits;
+template <> struct ExactTraits<float> {
+  static constexpr int kLsb = -149;    // 2^-149: the fp32 subnormal unit
+  static constexpr int kWords = 12;    // 384 bits >= 128 + 149 + 40 (n < 2^40) + sign
+  static constexpr int kPrec = 24;
+  static constexpr uint64_t kInfBits = 0x7f800000ull;
+  static constexpr uint64_t kSignBit = 0x80000000ull;
+  static constexpr uint64_t kQNaN = 0x7fc00000ull;
+};
+template <> struct ExactTraits<double> {
+  static constexpr int kLsb = -1074;   // 2^-1074: the fp64 subnormal unit
+  static constexpr int kWords = 68;    // 2176 bits >= 1024 + 1074 + 40 + sign
+  static constexpr int kPrec = 53;
+  static constexpr uint64_t kInfBits = 0x7ff0000000000000ull;
+  static constexpr uint64_t kSignBit = 0x8000000000000000ull;
+  static constexpr uint64_t kQNaN = 0x7ff8000000000000ull;
+};
+static_assert(ExactTraits<double>::kWords <= RD_EXACT_MAX_WORDS, "rd_exact_record too small");
+
+constexpr uint32_t kXNaN = 1u, kXPosInf = 2u, kXNegInf = 4u, kXNotNegZero = 8u;
+constexpr uint64_t kNegZeroBits = 0x8000000000000000ull;
+
+struct XArgs {
+  const unsigned char* x;
+  uint64_t n, head, nvec, tail_start, tail;
+  void* out;                 // mode 0: one element
+  rd_exact_record* rec;      // mode 1: one exact record
+  long long* partials;       // gridDim.x slots of (kWords + 1) words
+  unsigned* ticket;
+  uint32_t tag;
+  int mode;
+};
+
+// ------------------------------------------------------------ superaccumulator
+// w[k] += v (carry-save). A word whose magnitude passes 2^60 hands its high
+// part to w[k+1]: both are atomic adds of opposite value, so the represented
+// number never changes, whatever other lanes do meanwhile.
+template <int NW>
+__device__ __forceinline__ void sacc_word_add(long long* w, int k, long long v) {
+  for (;;) {
+    const long long now = (long long)atomicAdd((unsigned long long*)&w[k], (unsigned long long)v) + v;
+    if (k == NW - 1 || (now < (1ll << 60) && now > -(1ll << 60))) return;
+    const long long c = now >> 32;   // arithmetic shift
+    atomicAdd((unsigned long long*)&w[k], (unsigned long long)(-(c << 32)));
+    ++k;
+    v = c;
+  }
+}
+
+// deposit a finite double d exactly: d = +-m * 2^(e-1075), m < 2^53
+template <typename T>
+__device__ __forceinline__ void sacc_add(long long* w, double d) {
+  using TR = ExactTraits<T>;
+  const uint64_t b = (uint64_t)__double_as_longlong(d);
+  int e = (int)((b >> 52) & 0x7ff);
+  uint64_t m = b & ((1ull << 52) - 1);
+  if (e) m |= 1ull << 52;
+  else e = 1;
+  if (m == 0) return;
+  int p = e - 1075 - TR::kLsb;       // bit position of m's unit
+  if (p < 0) { m >>= -p; p = 0; }    // only zero bits (d is a multiple of 2^kLsb)
+  const int k = p >> 5, r = p & 31;
+  const uint64_t lo = m << r;
+  const long long d0 = (long long)(lo & 0xffffffffull), d1 = (long long)(lo >> 32);
+  const long long d2 = r ? (long long)(m >> (64 - r)) : 0;
+  const bool neg = (int64_t)b < 0;
+  if (d0) sacc_word_add<TR::kWords>(w, k, neg ? -d0 : d0);
+  if (d1) sacc_word_add<TR::kWords>(w, k + 1, neg ? -d1 : d1);
+  if (d2) sacc_word_add<TR::kWords>(w, k + 2, neg ? -d2 : d2);
+}
+
+// carry the words into digits [0, 2^32) (the top word keeps the sign); one thread
+template <int NW>
+__device__ __forceinline__ void sacc_normalise(long long* w) {
+  long long c = 0;
+  for (int k = 0; k < NW - 1; ++k) {
+    const long long t = w[k] + c;
+    w[k] = t & 0xffffffffll;
+    c = t >> 32;
+  }
+  w[NW - 1] += c;
+}
+
+// ------------------------------------------------------------------ expansions
+struct Ex { double a0, a1, a2; };   // a0 + a1 + a2 exactly; |a0| >> |a1| >> |a2| in practice
+
+// TwoSum (Knuth): s + e == a + b exactly (when s is finite)
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bp = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bp)), __dsub_rn(b, bp));
+}
+
+// the rare cases, out of line (keeps the hot loop small): an inf/NaN term,
+// an fp64 overflow of a0 + x, or a nonzero error of the second TwoSum, which
+// goes into a2 by a third TwoSum; only a third nonzero error reaches the
+// superaccumulator. Recomputes from the state before the element.
+struct ExSlow { Ex ex; uint32_t flags; };
+template <typename T>
+__device__ __noinline__ ExSlow ex_slow(Ex ex, double x, long long* w, uint32_t flags) {
+  if (!(fabs(x) <= 1.7976931348623157e308)) {   // inf or NaN term: flags only
+    flags |= (x != x) ? kXNaN : (x > 0 ? kXPosInf : kXNegInf);
+    return ExSlow{ex, flags};
+  }
+  flags |= kXNotNegZero;
+  double s, e;
+  two_sum(ex.a0, x, s, e);
+  if (!(fabs(s) <= 1.7976931348623157e308)) {   // a0 + x overflows (fp64 data): deposit x
+    sacc_add<T>(w, x);
+    return ExSlow{ex, flags};
+  }
+  ex.a0 = s;
+  if (e == 0.0) return ExSlow{ex, flags};
+  double s1, e1;
+  two_sum(ex.a1, e, s1, e1);
+  if (!(fabs(s1) <= 1.7976931348623157e308)) {
+    sacc_add<T>(w, e);
+    return ExSlow{ex, flags};
+  }
+  ex.a1 = s1;
+  if (e1 == 0.0) return ExSlow{ex, flags};
+  double s2, e2;
+  two_sum(ex.a2, e1, s2, e2);
+  if (!(fabs(s2) <= 1.7976931348623157e308)) {
+    sacc_add<T>(w, e1);
+    return ExSlow{ex, flags};
+  }
+  ex.a2 = s2;
+  if (e2 != 0.0) sacc_add<T>(w, e2);
+  return ExSlow{ex, flags};
+}
+
+// a0 + x = s + e exactly (TwoSum). e == 0: done (fp32 data with a narrow
+// exponent spread: nearly every term). Else e -- finite and nonzero unless x
+// is inf/NaN or s overflowed -- goes into a1 by a second TwoSum, inline (fp64
+// data: most terms); only a nonzero second error or a non-finite value leaves
+// the inline path.
+template <typename T>
+__device__ __forceinline__ void ex_add(Ex& ex, double x, long long* w, uint32_t& flags) {
+  double s, e;
+  two_sum(ex.a0, x, s, e);
+  if (__builtin_expect(e == 0.0, 1)) {
+    ex.a0 = s;
+    return;
+  }
+  double s1, e1;
+  two_sum(ex.a1, e, s1, e1);                     // NaN throughout for the non-finite cases
+  if (__builtin_expect(e1 == 0.0 && fabs(s1) <= 1.7976931348623157e308, 1)) {
+    ex.a0 = s;
+    ex.a1 = s1;
+    flags |= kXNotNegZero;                       // e != 0: x is not a zero
+    return;
+  }
+  const ExSlow r = ex_slow<T>(ex, x, w, flags);
+  ex = r.ex;
+  flags = r.flags;
+}
+
+template <typename T>
+__device__ __forceinline__ double widen(T v) { return (double)v; }   // exact for fp32
+
+// One loaded vector, speculatively and branch-free: every element's TwoSum(s)
+// are computed on the lane's expansion (the E expansions are independent
+// dependency chains) and their "inexact / non-finite" tests OR-ed; ONE branch
+// per vector. fp32 data: one TwoSum per element, speculating e == 0 (every
+// term of a narrow-exponent workload). fp64 data: both TwoSums, speculating
+// that the second error is 0 (a 53-bit term almost always leaves an error in
+// a0, almost never in a1). If the speculation fails the vector is replayed
+// element by element from the saved state through ex_add.
+template <int L>
+struct ExVals { double v[L]; };
+
+// two-level speculation over one vector: both TwoSums per element, branch-free
+template <int E, int L>
+__device__ __forceinline__ bool spec2(Ex (&ex)[E], const double (&xs)[L]) {
+  bool bad = false;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    Ex& q = ex[l % E];
+    double s, e, s1, e1;
+    two_sum(q.a0, xs[l], s, e);
+    two_sum(q.a1, e, s1, e1);
+    bad |= !(e1 == 0.0 && fabs(s1) <= 1.7976931348623157e308);   // NaN for inf/NaN/overflow
+    q.a0 = s;
+    q.a1 = s1;
+  }
+  return bad;
+}
+
+// the replay of a vector whose speculation failed, out of line: one copy of
+// this code for the whole kernel (inlined into every unrolled vector slot it
+// thrashed the instruction cache whenever it ran)
+template <int E, int L>
+struct ExState { Ex ex[E]; uint32_t flags; };
+template <typename T, int E, int L>
+__device__ __noinline__ ExState<E, L> replay_vec(ExState<E, L> st, const ExVals<L> xs, long long* w) {
+#pragma unroll
+  for (int l = 0; l < L; ++l) ex_add<T>(st.ex[l % E], xs.v[l], w, st.flags);
+  return st;
+}
+
+template <typename T, int E, int L>
+__device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L], long long* w,
+                                               uint32_t& flags) {
+  Ex save[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) save[j] = ex[j];
+  bool bad = false;
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int l = 0; l < L; ++l) {                // one TwoSum per element, speculating e == 0
+      Ex& q = ex[l % E];
+      double s, e;
+      two_sum(q.a0, xs[l], s, e);
+      bad |= (e != 0.0);                         // NaN (inf/NaN term) counts as failed
+      q.a0 = s;
+    }
+    if (__builtin_expect(!bad, 1)) return;
+#pragma unroll
+    for (int j = 0; j < E; ++j) ex[j] = save[j];
+  }
+  bad = spec2<E, L>(ex, xs);
+  if (__builtin_expect(bad, 0)) {                // replay element by element
+    ExState<E, L> st;
+#pragma unroll
+    for (int j = 0; j < E; ++j) st.ex[j] = save[j];
+    st.flags = flags;
+    ExVals<L> v;
+#pragma unroll
+    for (int l = 0; l < L; ++l) v.v[l] = xs[l];
+    st = replay_vec<T, E, L>(st, v, w);
+#pragma unroll
+    for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
+    flags = st.flags;
+  }
+}
+
+// round the normalised words (value = sum w[k] 2^(32k) * 2^kLsb) once; returns the float's bits
+template <typename T>
+__device__ uint64_t exact_round(const long long* w, uint32_t flags, uint64_t n) {
+  using TR = ExactTraits<T>;
+  constexpr int NW = TR::kWords, p = TR::kPrec;
+  if ((flags & kXNaN) || ((flags & kXPosInf) && (flags & kXNegInf))) return TR::kQNaN;
+  if (flags & kXPosInf) return TR::kInfBits;
+  if (flags & kXNegInf) return TR::kInfBits | TR::kSignBit;
+  const bool neg = w[NW - 1] < 0;
+  uint32_t D[NW];
+  uint64_t c = neg ? 1 : 0;
+  for (int k = 0; k < NW; ++k) {                // magnitude digits (two's complement negation)
+    const uint32_t dk = (uint32_t)w[k];
+    const uint64_t t = (uint64_t)(neg ? ~dk : dk) + c;
+    D[k] = (uint32_t)t;
+    c = neg ? (t >> 32) : 0;
+  }
+  int kt = NW - 1;
+  while (kt >= 0 && D[kt] == 0) --kt;
+  if (kt < 0) return (n == 0 || (flags & kXNotNegZero)) ? 0ull : TR::kSignBit;   // exact zero (R2)
+  const int lz = __clz(D[kt]);
+  const int P = 32 * kt + 31 - lz;              // leading one
+  uint64_t bits;
+  if (P < p) {
+    // the integer itself is the bit pattern: subnormal (exponent field 0) or
+    // the smallest normal binade (field 1 = the 2^(p-1) bit)
+    bits = ((uint64_t)(kt >= 1 ? D[1] : 0) << 32) | D[0];
+  } else {
+    const uint32_t Dm1 = kt >= 1 ? D[kt - 1] : 0, Dm2 = kt >= 2 ? D[kt - 2] : 0;
+    const unsigned __int128 win = ((unsigned __int128)D[kt] << 64) | ((unsigned __int128)Dm1 << 32) | Dm2;
+    const int sh = 32 - lz;                     // 96-bit window -> leading one at bit 63
+    const uint64_t W64 = (uint64_t)(win >> sh);
+    bool sticky = ((uint64_t)win & ((1ull << sh) - 1)) != 0;
+    for (int k = 0; k < kt - 2 && !sticky; ++k) sticky = D[k] != 0;
+    uint64_t q = W64 >> (64 - p);
+    const bool guard = (W64 >> (63 - p)) & 1;
+    const bool rest = (W64 & ((1ull << (63 - p)) - 1)) != 0 || sticky;
+    if (guard && (rest || (q & 1))) ++q;        // ties to even
+    bits = ((uint64_t)(P + 1 - p) << (p - 1)) + q;   // a carry out of q bumps the exponent
+    if (bits >= TR::kInfBits) bits = TR::kInfBits;   // beyond the range: inf (IEEE overflow)
+  }
+  return neg ? (bits | TR::kSignBit) : bits;
+}
+
+template <typename T>
+__device__ __forceinline__ void exact_store(const long long* w, uint32_t flags, uint64_t n, void* out) {
+  const uint64_t b = exact_round<T>(w, flags, n);
+  if constexpr (sizeof(T) == 4) *(uint32_t*)out = (uint32_t)b;
+  else *(uint64_t*)out = b;
+}
+
+// --------------------------------------------------------------------- kernel
+template <typename T, int B, int U, int E, int MINB>
+__global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
+  using TR = ExactTraits<T>;
+  constexpr int NW = TR::kWords;
+  constexpr int VB = 32;
+  constexpr int L = VB / (int)sizeof(T);
+  constexpr int NWARP = B / 32;
+  __shared__ long long sacc[NWARP][NW];
+  __shared__ long long tot[B];
+  __shared__ unsigned s_flags, s_last;
+
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_flags = 0;
+  __syncthreads();
+  long long* w = sacc[warp];
+
+  Ex ex[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) ex[j] = Ex{-0.0, -0.0, -0.0};
+  uint32_t flags = 0;
+
+  const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * B;
+  const unsigned char* body = args.x + args.head * sizeof(T);
+  pdl_wait();
+  const uint64_t nvec = args.nvec;
+  uint64_t i = tid;
+  // The main loop's trip count is warp-uniform (tested on the warp's last
+  // lane, whose index is the largest), so every iteration can end with a
+  // __syncwarp: a lane that replayed a vector (divergent) rejoins its warp
+  // there. Without it the warp stayed split after the first divergent replay
+  // and ran the loop ~2 lanes at a time (ncu: 2.0 avg threads per F2F).
+  const uint64_t lag = 31 - (uint64_t)ln;        // lane 31's index = i + lag
+  for (; i + lag + (uint64_t)(U - 1) * stride < nvec; i += (uint64_t)U * stride) {
+    Vec<VB> v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double xs[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v[u], l));
+      fold_vec_exact<T, E, L>(ex, xs, w, flags);
+    }
+    __syncwarp();
+  }
+  for (; i < nvec; i += stride) {
+    Vec<VB> v = ldg_stream<VB>(body + i * VB);
+    double xs[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v, l));
+    fold_vec_exact<T, E, L>(ex, xs, w, flags);
+  }
+  pdl_trigger();
+  // a2: head and tail stragglers
+  if (tid < args.head) ex_add<T>(ex[0], widen(ldg_scalar<T>(args.x + tid * sizeof(T))), w, flags);
+  if (tid < args.tail) ex_add<T>(ex[1], widen(ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T))), w, flags);
+  // a3: the expansions into the warp's superaccumulator. Every term passes
+  // through some a0 (or the slow path, which flags itself), and an a0 that
+  // has seen a term other than -0.0 is never -0.0 again (x + -x = +0), so a0
+  // alone decides reading R2's "every term is -0.0".
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    if ((uint64_t)__double_as_longlong(ex[j].a0) != kNegZeroBits) flags |= kXNotNegZero;
+    if (ex[j].a0 != 0.0) sacc_add<T>(w, ex[j].a0);
+    if (ex[j].a1 != 0.0) sacc_add<T>(w, ex[j].a1);
+    if (ex[j].a2 != 0.0) sacc_add<T>(w, ex[j].a2);
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (ln == 0 && flags) atomicOr(&s_flags, flags);
+  __syncwarp();
+  // a4: each warp carries its words into digits
+  if (ln == 0) sacc_normalise<NW>(w);
+  __syncthreads();
+  // a5: the CTA's words (sum of NWARP digit vectors: < 2^35 per word)
+  long long* slot = args.partials + (size_t)blockIdx.x * (NW + 1);
+  if (threadIdx.x < NW) {
+    long long s = 0;
+#pragma unroll
+    for (int q = 0; q < NWARP; ++q) s += sacc[q][threadIdx.x];
+    __stcg(slot + threadIdx.x, s);
+  }
+  if (threadIdx.x == NW) __stcg(slot + NW, (long long)s_flags);
+  // a6: last CTA adds the G slots
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(args.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int G = (int)gridDim.x;
+  constexpr int GROUPS = B / (NW + 1);             // (word, slot-group) pairs in parallel
+  if (threadIdx.x < GROUPS * (NW + 1)) {
+    const int j = threadIdx.x % (NW + 1), grp = threadIdx.x / (NW + 1);
+    long long s = 0;
+    for (int g = grp; g < G; g += GROUPS) {
+      const long long v = __ldcg(args.partials + (size_t)g * (NW + 1) + j);
+      s = (j == NW) ? (s | v) : (s + v);           // the flags word is OR-ed
+    }
+    tot[threadIdx.x] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x <= NW) {
+    const int j = threadIdx.x;
+    long long s = 0;
+    for (int grp = 0; grp < GROUPS; ++grp) {
+      const long long v = tot[grp * (NW + 1) + j];
+      s = (j == NW) ? (s | v) : (s + v);
+    }
+    if (j < NW) sacc[0][j] = s;
+    else s_flags = (unsigned)s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sacc_normalise<NW>(sacc[0]);
+    *args.ticket = 0u;
+    if (args.mode == 0) {
+      exact_store<T>(sacc[0], s_flags, args.n, args.out);
+    } else {
+      rd_exact_record* r = args.rec;
+      r->tag = args.tag;
+      r->status = 0;
+      r->n = args.n;
+      r->flags = s_flags;
+      r->nwords = NW;
+      r->reserved = 0;
+      for (int k = 0; k < NW; ++k) r->word[k] = sacc[0][k];
+      for (int k = NW; k < RD_EXACT_MAX_WORDS; ++k) r->word[k] = 0;
+    }
+  }
+}
+
+// Fold `count` exact records (any order gives the same integer): one CTA.
+template <typename T>
+__global__ void rd_exact_combine_kernel(const rd_exact_record* recs, int count, uint32_t tag, void* out,
+                                        rd_exact_record* rec_out, int* d_status) {
+  using TR = ExactTraits<T>;
+  constexpr int NW = TR::kWords;
+  __shared__ long long s[NW];
+  __shared__ unsigned s_flags, s_bad;
+  __shared__ unsigned long long s_n;
+  if (threadIdx.x == 0) { s_flags = 0; s_bad = 0; s_n = 0; }
+  __syncthreads();
+  for (int r = threadIdx.x; r < count; r += blockDim.x) {
+    const rd_exact_record* q = recs + r;
+    if (q->tag != tag || q->nwords != (uint32_t)NW) atomicOr(&s_bad, 1u);
+    else {
+      atomicOr(&s_flags, q->flags);
+      atomicAdd(&s_n, (unsigned long long)q->n);
+    }
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < NW) {
+    long long a = 0;
+    for (int r = 0; r < count; ++r)
+      if (recs[r].tag == tag && recs[r].nwords == (uint32_t)NW) a += recs[r].word[threadIdx.x];
+    s[threadIdx.x] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  sacc_normalise<NW>(s);
+  if (s_bad && d_status) *d_status = (int)RD_ERR_MISMATCH;
+  if (out) {
+    if (s_bad || s_n == 0) {
+      if constexpr (sizeof(T) == 4) *(uint32_t*)out = 0u;
+      else *(uint64_t*)out = 0ull;
+    } else {
+      exact_store<T>(s, s_flags, s_n, out);
+    }
+  }
+  if (rec_out) {
+    rec_out->tag = tag;
+    rec_out->status = s_bad ? (uint32_t)RD_ERR_MISMATCH : 0u;
+    rec_out->n = s_n;
+    rec_out->flags = s_flags;
+    rec_out->nwords = NW;
+    rec_out->reserved = 0;
+    for (int k = 0; k < NW; ++k) rec_out->word[k] = s[k];
+    for (int k = NW; k < RD_EXACT_MAX_WORDS; ++k) rec_out->word[k] = 0;
+  }
+}
+
+}  // namespace rd

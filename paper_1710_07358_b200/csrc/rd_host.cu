@@ -24,6 +24,8 @@ struct HostPipe {
   void* stage[2] = {nullptr, nullptr};
   rd_record* recs = nullptr;
   int rec_cap = 0;
+  rd_exact_record* xrecs = nullptr;   // RD_SUM_EXACT on floats
+  int xrec_cap = 0;
   void* d_out = nullptr;
   std::mutex mu;
 };
@@ -73,6 +75,7 @@ void release_host_pipelines() {
       cudaEventDestroy(p->consumed[b]);
     }
     cudaFree(p->recs);
+    cudaFree(p->xrecs);
     cudaFree(p->d_out);
     cudaStreamDestroy(p->copy);
     cudaStreamDestroy(p->comp);
@@ -109,6 +112,15 @@ extern "C" rd_status reduce_host(const void* x_host, size_t n, rd_dtype dtype, r
     if ((e = cudaMalloc(&p->recs, sizeof(rd_record) * cap)) != cudaSuccess) return cuda_fail(e, "records cudaMalloc");
     p->rec_cap = cap;
   }
+  const bool exact = is_exact_float(dtype, op);
+  if (exact && nchunks > (uint64_t)p->xrec_cap) {
+    if (p->xrecs) cudaFree(p->xrecs);
+    p->xrecs = nullptr;
+    p->xrec_cap = 0;
+    int cap = (int)(nchunks < 64 ? 64 : nchunks);
+    if ((e = cudaMalloc(&p->xrecs, sizeof(rd_exact_record) * cap)) != cudaSuccess) return cuda_fail(e, "records cudaMalloc");
+    p->xrec_cap = cap;
+  }
   const unsigned char* src = (const unsigned char*)x_host;
   for (uint64_t k = 0; k < nchunks; ++k) {
     const int b = (int)(k & 1);
@@ -119,11 +131,13 @@ extern "C" rd_status reduce_host(const void* x_host, size_t n, rd_dtype dtype, r
       return cuda_fail(e, "H2D copy");
     if ((e = cudaEventRecord(p->copied[b], p->copy)) != cudaSuccess) return cuda_fail(e, "event record");
     if ((e = cudaStreamWaitEvent(p->comp, p->copied[b], 0)) != cudaSuccess) return cuda_fail(e, "wait");
-    st = launch_reduce(p->stage[b], len / s, dtype, op, 1, nullptr, p->recs + k, p->comp, nullptr, nullptr);
+    st = exact ? launch_exact(p->stage[b], len / s, dtype, 1, nullptr, p->xrecs + k, p->comp, nullptr, nullptr)
+               : launch_reduce(p->stage[b], len / s, dtype, op, 1, nullptr, p->recs + k, p->comp, nullptr, nullptr);
     if (st != RD_OK) return st;
     if ((e = cudaEventRecord(p->consumed[b], p->comp)) != cudaSuccess) return cuda_fail(e, "event record");
   }
-  st = launch_combine(p->recs, (int)nchunks, dtype, op, p->d_out, nullptr, nullptr, p->comp);
+  st = exact ? launch_exact_combine(p->xrecs, (int)nchunks, dtype, p->d_out, nullptr, nullptr, p->comp)
+             : launch_combine(p->recs, (int)nchunks, dtype, op, p->d_out, nullptr, nullptr, p->comp);
   if (st != RD_OK) return st;
   if ((e = cudaMemcpyAsync(out_host, p->d_out, out_size(dtype, op), cudaMemcpyDeviceToHost, p->comp)) != cudaSuccess)
     return cuda_fail(e, "D2H copy");

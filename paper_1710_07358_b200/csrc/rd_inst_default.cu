@@ -17,6 +17,7 @@ bool lookup_int(int dtype, int op, int variant, int unroll, int vec_bytes, Kerne
       RD_CASE_DEFAULT(DT, RD_XOR)                                               \
       RD_CASE_DEFAULT(DT, RD_ARGMIN) RD_CASE_DEFAULT(DT, RD_ARGMAX)             \
       RD_CASE_DEFAULT(DT, RD_SUM_COMPENSATED)                                   \
+      RD_CASE_DEFAULT(DT, RD_SUM_EXACT)                                         \
       default: return false;                                                    \
     }
   switch (dtype) {
@@ -51,7 +52,7 @@ CombineFn lookup_combine(int dtype, int op) {
   if (dtype == DT && op == OP) return rd_combine_kernel<typename OpFor<DT, OP>::type>;
 #define RD_C_INT(DT) RD_C(DT, RD_SUM) RD_C(DT, RD_PROD) RD_C(DT, RD_MIN) RD_C(DT, RD_MAX) \
   RD_C(DT, RD_AND) RD_C(DT, RD_OR) RD_C(DT, RD_XOR) RD_C(DT, RD_ARGMIN) RD_C(DT, RD_ARGMAX)   \
-  RD_C(DT, RD_SUM_COMPENSATED)
+  RD_C(DT, RD_SUM_COMPENSATED) RD_C(DT, RD_SUM_EXACT)
 #define RD_C_FLT(DT) RD_C(DT, RD_SUM) RD_C(DT, RD_PROD) RD_C(DT, RD_MIN) RD_C(DT, RD_MAX) \
   RD_C(DT, RD_ARGMIN) RD_C(DT, RD_ARGMAX) RD_C(DT, RD_SUM_COMPENSATED)
   RD_C_INT(RD_INT32) RD_C_INT(RD_UINT32) RD_C_INT(RD_INT64)

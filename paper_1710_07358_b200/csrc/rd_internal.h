@@ -17,6 +17,7 @@ rd_status cuda_fail(cudaError_t e, const char* what);
 rd_status check_dtype_op(int dtype, int op);
 int dtype_size(int dtype);
 bool is_arg_op(int op);
+bool is_exact_float(int dtype, int op);   // RD_SUM_EXACT on float32/float64
 int out_size(int dtype, int op);   // bytes of one result: element, or rd_arg_result
 
 struct Mailbox;
@@ -34,6 +35,13 @@ struct FusedArgs {
 rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, void* out,
                         rd_record* rec, cudaStream_t stream, const rd_config* cfg,
                         rd_launch_info* info, const FusedArgs* fused = nullptr);
+
+// RD_SUM_EXACT on floats (rd_exact.cuh): mode 0 -> one element at `out`,
+// mode 1 -> one rd_exact_record at `xrec`; and the exact-record combine.
+rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, rd_exact_record* xrec,
+                       cudaStream_t stream, const rd_config* cfg, rd_launch_info* info);
+rd_status launch_exact_combine(const rd_exact_record* recs, int count, int dtype, void* out,
+                               rd_exact_record* rec_out, int* d_status, cudaStream_t stream);
 
 // Launch the record-combine kernel (N4).
 rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, void* out,

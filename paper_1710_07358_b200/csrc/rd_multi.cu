@@ -23,6 +23,8 @@ struct rd_comm {
   rd_record* d_send = nullptr;   // this rank's record
   rd_record* d_recv = nullptr;   // nranks records, rank order
   int* d_err = nullptr;          // sticky mismatch flag (rd_comm_check clears it)
+  rd_exact_record* d_xsend = nullptr;   // RD_SUM_EXACT on floats: this rank's exact record
+  rd_exact_record* d_xrecv = nullptr;   // nranks exact records
 };
 
 namespace {
@@ -67,6 +69,19 @@ rd_status rd_comm_init(rd_comm_t* comm, int nranks, int rank, const rd_unique_id
   c->d_send = (rd_record*)p;
   c->d_recv = c->d_send + 1;
   c->d_err = (int*)(c->d_recv + nranks);
+  void* q = nullptr;
+  e = cudaMalloc(&q, sizeof(rd_exact_record) * (nranks + 1));
+  if (e == cudaSuccess) e = cudaMemset(q, 0, sizeof(rd_exact_record) * (nranks + 1));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (q) cudaFree(q);
+    cudaFree(p);
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return rd::cuda_fail(e, "exact comm buffers");
+  }
+  c->d_xsend = (rd_exact_record*)q;
+  c->d_xrecv = c->d_xsend + 1;
   *comm = c;
   return RD_OK;
 }
@@ -77,6 +92,7 @@ rd_status rd_comm_destroy(rd_comm_t comm) {
   cudaDeviceSynchronize();
   ncclResult_t r = ncclCommDestroy(comm->nccl);
   cudaFree(comm->d_send);
+  cudaFree(comm->d_xsend);
   delete comm;
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
   return RD_OK;
@@ -90,6 +106,20 @@ rd_status reduce_multi(const void* x_local, size_t n_local, rd_dtype dtype, rd_o
   if (st != RD_OK) return st;
   if ((uintptr_t)out % (rd::is_arg_op(op) ? 8 : rd::dtype_size(dtype))) { rd::set_error("out misaligned"); return RD_ERR_MISALIGNED; }
   cudaStream_t s = (cudaStream_t)stream;
+  if (rd::is_exact_float(dtype, op)) {
+    // exact sum: the local shard's exact record (608 B), all-gathered; the W
+    // fixed-point integers add exactly, so every rank and every W gives the
+    // same bits (reading R17)
+    st = rd::launch_exact(x_local, n_local, dtype, 1, nullptr, comm->d_xsend, s, nullptr, nullptr);
+    if (st != RD_OK) return st;
+    const rd_exact_record* recs = comm->d_xsend;
+    if (comm->nranks > 1) {
+      ncclResult_t r = ncclAllGather(comm->d_xsend, comm->d_xrecv, sizeof(rd_exact_record), ncclUint8, comm->nccl, s);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+      recs = comm->d_xrecv;
+    }
+    return rd::launch_exact_combine(recs, comm->nranks, dtype, out, nullptr, comm->d_err, s);
+  }
   // a0-a7 on the local shard -> this rank's record
   st = rd::launch_reduce(x_local, n_local, dtype, op, 1, nullptr, comm->d_send, s, nullptr, nullptr);
   if (st != RD_OK) return st;

@@ -568,6 +568,10 @@ RD_ARG_OPS(RD_FLOAT64, uint64_t)
 template <> struct OpFor<RD_INT32, RD_SUM_COMPENSATED> { using type = IntOp<uint32_t, RD_SUM, true>; };
 template <> struct OpFor<RD_UINT32, RD_SUM_COMPENSATED> { using type = IntOp<uint32_t, RD_SUM, false>; };
 template <> struct OpFor<RD_INT64, RD_SUM_COMPENSATED> { using type = IntOp<uint64_t, RD_SUM, true>; };
+// exact sum (rd_exact.cuh for floats): integer sums are exact already
+template <> struct OpFor<RD_INT32, RD_SUM_EXACT> { using type = IntOp<uint32_t, RD_SUM, true>; };
+template <> struct OpFor<RD_UINT32, RD_SUM_EXACT> { using type = IntOp<uint32_t, RD_SUM, false>; };
+template <> struct OpFor<RD_INT64, RD_SUM_EXACT> { using type = IntOp<uint64_t, RD_SUM, true>; };
 template <> struct OpFor<RD_FLOAT32, RD_SUM_COMPENSATED> { using type = Float32SumComp; };
 template <> struct OpFor<RD_FLOAT64, RD_SUM_COMPENSATED> { using type = Float64SumComp; };
 template <> struct OpFor<RD_FLOAT32, RD_SUM> { using type = FloatSum<float>; };

@@ -28,6 +28,21 @@ bool lookup_float(int dtype, int op, int variant, int unroll, int vec_bytes, Ker
 bool lookup_ablation(int dtype, int op, int variant, int unroll, int vec_bytes, KernelRef* r);
 CombineFn lookup_combine(int dtype, int op);
 
+// exact float sum (RD_SUM_EXACT, rd_exact.cuh): one vector-load kernel per
+// float dtype, launched by launch_exact (rd_api.cu)
+struct XArgs;
+using ExactFn = void (*)(const XArgs);
+using ExactCombineFn = void (*)(const rd_exact_record*, int, uint32_t, void*, rd_exact_record*, int*);
+struct ExactRef {
+  ExactFn fn;
+  int block, unroll, vec_bytes;
+};
+constexpr int kExactUnroll = 6;       // 32-byte loads in flight per thread per iteration (tools/tune_exact.py)
+constexpr int kExactExpansions = 2;   // independent (a0, a1) expansions per thread
+constexpr int kExactMinBlocks = 1;    // __launch_bounds__ min CTAs/SM (register cap)
+bool lookup_exact(int dtype, ExactRef* r);
+ExactCombineFn lookup_exact_combine(int dtype);
+
 // bulk variant: CW consumer warps + 1 producer warp per CTA. 8 consumer warps
 // keep up with HBM for the cheap combiners; the ALU-heavier float argmin /
 // argmax folds get 16 (more warps to hide the dependent integer chains).

@@ -2,6 +2,7 @@
 
 - integers, all ops: bit-exact;
 - float min/max: bit-exact (NaN compared as "is NaN");
+- float sum_exact: bit-exact (the exact sum rounded once is unique; reading R17);
 - float sum: |gpu - exact| <= 4 * eps(dtype) * sum|x_i|  (BASELINE.json north_star),
   where exact = oracle's unrounded hi + lo; a zero sum of zeros compares the sign bit;
 - float prod: |gpu - exact| <= 4 * eps(dtype) * |exact| (the analogous bound);
@@ -39,7 +40,7 @@ def check(got, x: np.ndarray, op: str, ref=None, factor: float = 4.0):
             assert to_bits(g, dtype) == to_bits(r.value, dtype), f"{op}: value {g!r} want {r.value!r}"
         return r
     g = np.array([got], dtype=x.dtype)[0]
-    if not dtype.startswith("float") or op in ("min", "max"):
+    if not dtype.startswith("float") or op in ("min", "max", "sum_exact"):
         if dtype.startswith("float") and math.isnan(float(r.value)):
             assert math.isnan(float(g)), f"{op}: want NaN, got {g}"
             return r

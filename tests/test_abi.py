@@ -40,7 +40,7 @@ def test_header_declares_the_boundary():
                  "rd_identity", "rd_release_workspaces", "rd_status_string", "rd_last_error",
                  "rd_shard_range", "rd_reduce_ex", "reduce_fused", "rd_fused_create",
                  "rd_fused_connect", "rd_fused_connect_local", "rd_fused_mailbox", "rd_fused_check",
-                 "rd_fused_destroy"]:
+                 "rd_fused_destroy", "reduce_exact_partial", "rd_combine_exact_records"]:
         assert must in names, must
 
 
@@ -54,6 +54,8 @@ def test_library_exports_every_declared_symbol():
 def test_record_layout():
     assert ctypes.sizeof(_lib.rd_record) == 32 == rd.RECORD_BYTES
     assert ctypes.sizeof(_lib.rd_unique_id) == 128
+    assert ctypes.sizeof(_lib.rd_exact_record) == 608 == rd.EXACT_RECORD_BYTES
+    assert _lib.rd_exact_record.word.offset == 32
 
 
 def test_status_strings():
@@ -92,7 +94,16 @@ def test_validation_before_any_device_work():
     assert L.reduce(None, 5, 0, 0, out, None) == 1                 # x NULL, n > 0
     assert L.reduce(p, 5, 0, 0, None, None) == 1                   # out NULL
     assert L.reduce(p, 5, 9, 0, out, None) == 1                    # unknown dtype
-    assert L.reduce(p, 5, 0, 10, out, None) == 1                   # unknown op
+    assert L.reduce(p, 5, 0, 11, out, None) == 1                   # unknown op
+    assert L.reduce_partial(p, 5, 3, 10, out, None) == 2           # exact float partial needs a wide record
+    assert L.rd_combine_records(p, 1, 4, 10, out, None, None, None) == 2
+    assert L.reduce_fused(p, 4, 3, 10, out, None, None) == 1        # comm NULL comes first
+    assert L.reduce_exact_partial(p, 5, 0, out, None) == 2         # integer dtype: use reduce_partial
+    assert L.reduce_exact_partial(None, 5, 3, out, None) == 1
+    assert L.reduce_exact_partial(p + 2, 5, 3, out, None) == 3
+    assert L.rd_combine_exact_records(p, 1, 2, out, None, None, None) == 2
+    assert L.rd_combine_exact_records(None, 2, 3, out, None, None, None) == 1
+    assert L.rd_combine_exact_records(p, 1, 3, None, None, None, None) == 1
     assert L.reduce(p, 5, 0, 7, ctypes.c_void_p(p + 4), None) == 3  # argmin result not 8-aligned
     for op in (4, 5, 6):
         assert L.reduce(p, 5, 3, op, out, None) == 2               # bitwise on float32

@@ -1,0 +1,177 @@
+"""Parity of the exact float sum (RD_SUM_EXACT, reading
+R17) with the oracle: the exact sum rounded once is unique, so every
+comparison is bit for bit -- across sizes, base offsets, grids, shard splits,
+the host path, the NCCL path, specials and full BASELINE sizes. Needs a B200."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+from tests import _parity
+from tests.test_gpu_parity import SIZES, to_dev, val
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FLT = ["float32", "float64"]
+WLS = ["u01", "normalish", "wide", "wide_full"]
+
+
+@pytest.fixture(scope="module")
+def rd():
+    from paper_1710_07358_b200.build import build_all
+    build_all()
+    import paper_1710_07358_b200 as m
+    return m
+
+
+def bits(v):
+    return np.asarray(v).tobytes()
+
+
+def same(g, want):
+    g, want = np.asarray(g), np.asarray(want)
+    if np.isnan(want):
+        return bool(np.isnan(g))
+    return g.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("dtype", FLT)
+@pytest.mark.parametrize("wl", WLS)
+def test_exact_sizes(rd, dtype, wl):
+    for n in SIZES:
+        x = inputs.generate(n, dtype, wl, seed=n % 5 + 1)
+        r = oracle.reduce(x, "sum_exact")
+        assert same(val(rd.reduce(to_dev(x), "sum_exact")), r.value), (dtype, wl, n)
+
+
+@pytest.mark.parametrize("dtype", FLT)
+def test_exact_offsets_grids_and_shards(rd, dtype):
+    """One result for every base offset, grid and split into records (reading R17)."""
+    n = (1 << 20) + 13
+    x = inputs.generate(n, dtype, "wide", seed=3)
+    want = oracle.reduce(x, "sum_exact").value
+    for off in range(8):
+        xd = to_dev(x, off)
+        assert same(val(rd.reduce(xd, "sum_exact")), want), off
+    xd = to_dev(x, 3)
+    for grid in (1, 2, 3, 7, 148, 296, 1000, 4096):
+        got, info = rd.reduce_ex(xd, "sum_exact", grid=grid)
+        assert info["grid"] == grid and same(val(got), want), grid
+    RB = rd.EXACT_RECORD_BYTES
+    for W in (1, 2, 3, 8, 17):
+        recs = torch.empty(W * RB, dtype=torch.uint8, device="cuda")
+        for r in range(W):
+            b, c = rd.shard_range(n, W, r)
+            rd.reduce_exact_partial(xd[b:b + c], rec=recs[r * RB:(r + 1) * RB])
+        assert same(val(rd.combine_exact_records(recs, dtype)), want), W
+        # records add in any order
+        perm = torch.randperm(W).tolist()
+        shuffled = torch.cat([recs[p * RB:(p + 1) * RB] for p in perm])
+        assert same(val(rd.combine_exact_records(shuffled, dtype)), want)
+        # a combined record combines again
+        rec2 = torch.empty(RB, dtype=torch.uint8, device="cuda")
+        rd.combine_exact_records(recs, dtype, rec_out=rec2)
+        assert same(val(rd.combine_exact_records(rec2, dtype)), want)
+
+
+@pytest.mark.parametrize("dtype", FLT)
+def test_exact_host_and_multi(rd, dtype):
+    n = (1 << 23) + 5                                   # several 32 MiB host chunks
+    x = inputs.generate(n, dtype, "wide", seed=4)
+    want = oracle.reduce(x, "sum_exact").value
+    assert same(rd.reduce_host(x, "sum_exact"), want)
+    assert same(rd.reduce_host(torch.from_numpy(x).pin_memory(), "sum_exact"), want)
+    import ctypes
+    from paper_1710_07358_b200 import _lib
+    L = _lib.lib()
+    uid = _lib.rd_unique_id()
+    assert L.rd_get_unique_id(ctypes.byref(uid)) == 0
+    h = ctypes.c_void_p()
+    assert L.rd_comm_init(ctypes.byref(h), 1, 0, ctypes.byref(uid), torch.cuda.current_device()) == 0
+    comm = rd.Comm(h.value, 1, 0, torch.cuda.current_device())
+    try:
+        assert same(val(comm.reduce(to_dev(x, 1), "sum_exact")), want)
+        comm.check()
+    finally:
+        comm.destroy()
+
+
+def _specials(dtype):
+    f = np.finfo(dtype)
+    big, tiny = f.max, f.smallest_subnormal
+    return [
+        [np.nan], [np.inf, 1.0], [-np.inf, 1.0], [np.inf, -np.inf], [1.0, np.nan, -np.inf],
+        [-0.0], [-0.0, -0.0, -0.0], [-0.0, 0.0], [1.0, -1.0], [0.0],
+        [big, big], [big, big, -big], [-big, -big], [big] * 5 + [-big] * 4,
+        [tiny] * 7, [tiny, -tiny], [1.5, 2.0 ** 100, -(2.0 ** 100)],     # P:50 fn 2
+        [1.0, 1e30, 1.0, -1e30], [1.0, 2.0 ** -24], [1.0, 2.0 ** -53], [1.0, 3 * 2.0 ** -24],
+    ]
+
+
+@pytest.mark.parametrize("dtype", FLT)
+def test_exact_specials(rd, dtype):
+    """Specials, signed zeros, overflow of the exact sum, subnormals, ties -- alone and
+    buried in a larger array (so they sit in the body, head and tail of the kernel)."""
+    with np.errstate(over="ignore"):
+        cases = [np.array(c, dtype=dtype) for c in _specials(dtype)]
+    for c in cases:
+        assert same(val(rd.reduce(to_dev(c), "sum_exact")), oracle.reduce(c, "sum_exact").value), c
+        for pos in (0, 5000, 10000 - c.size):
+            x = np.zeros(10000, dtype=dtype)
+            if c[0] == 0 and np.signbit(c[0]):
+                x[:] = -0.0                             # keep "every term is -0.0" cases intact
+            x[pos:pos + c.size] = c
+            assert same(val(rd.reduce(to_dev(x, 1), "sum_exact")), oracle.reduce(x, "sum_exact").value), (c, pos)
+
+
+@pytest.mark.parametrize("dtype", FLT)
+@pytest.mark.parametrize("wl", ["u01", "normalish", "wide"])
+def test_exact_full_size(rd, dtype, wl):
+    """BASELINE configs[1] size, n = 2^28: bit-exact vs the oracle; the same bits from a
+    forced grid and from an 8-way split (reading R17: reproducible across GPU counts)."""
+    n = 1 << 28
+    x = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
+    inputs.fill_device(x, wl, seed=1)
+    g = val(rd.reduce(x, "sum_exact"))
+    RB = rd.EXACT_RECORD_BYTES
+    recs = torch.empty(8 * RB, dtype=torch.uint8, device="cuda")
+    for r in range(8):
+        b, c = rd.shard_range(n, 8, r)
+        rd.reduce_exact_partial(x[b:b + c], rec=recs[r * RB:(r + 1) * RB])
+    alt = {bits(val(rd.combine_exact_records(recs, dtype))), bits(val(rd.reduce_ex(x, "sum_exact", grid=999)[0]))}
+    xh = x.cpu().numpy()
+    del x
+    want = oracle.reduce(xh, "sum_exact").value
+    assert same(g, want) and alt == {bits(g)}
+    if wl != "wide":   # exact sum within the 4 eps sum|x| bound of the plain sum's contract too
+        _parity.check(g, xh, "sum")
+
+
+def test_exact_integers_are_sum(rd):
+    for dt in ("int32", "uint32", "int64"):
+        x = inputs.generate(100003, dt, "uniform_bits", seed=2)
+        xd = to_dev(x, 1)
+        assert bits(val(rd.reduce(xd, "sum_exact"))) == bits(val(rd.reduce(xd, "sum")))
+        rec = rd.reduce_partial(xd, "sum_exact")
+        assert bits(val(rd.combine_records(rec, dt, "sum_exact"))) == bits(oracle.reduce(x, "sum").value)
+
+
+def test_exact_graph_capture(rd):
+    x = to_dev(inputs.generate(1 << 22, "float32", "wide", seed=9), 2)
+    want = val(rd.reduce(x, "sum_exact"))
+    out = torch.empty((), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        rd.reduce(x, "sum_exact", out=out)        # workspace for this stream outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        rd.reduce(x, "sum_exact", out=out)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert bits(val(out)) == bits(want)

@@ -40,6 +40,14 @@ def test_distributions():
     assert 0 < int((sc != 0xFFFFFFFF).sum()) < 64
     pm = inputs.generate(1 << 22, "float32", "sparse_pm1")
     assert 0 < int((pm != 0).sum()) <= (1 << 21)
+    for dt, lo, hi in (("float32", -40, 40), ("float64", -40, 40)):
+        w = inputs.generate(1 << 16, dt, "wide")
+        e = np.frexp(w)[1] - 1
+        assert e.min() == lo and e.max() == hi and abs((w < 0).mean() - 0.5) < 0.02
+    wf = inputs.generate(1 << 16, "float32", "wide_full")
+    assert np.isfinite(wf).all() and (np.abs(wf) < np.finfo(np.float32).tiny).any() and np.abs(wf).max() > 1e38
+    wd = inputs.generate(1 << 16, "float64", "wide_full")
+    assert np.isfinite(wd).all() and (np.abs(wd) < np.finfo(np.float64).tiny).any() and np.abs(wd).max() > 1e307
 
 
 def test_undefined_workloads_rejected():

@@ -15,12 +15,16 @@ import paper_1710_07358_b200 as rd  # noqa: E402
 
 PAIRS = [("int32", "sum"), ("float64", "sum"), ("float64", "prod"), ("float32", "max"),
          ("float32", "argmin"), ("float64", "sum_compensated")]
+# `python tools/profile_ops.py exact`: the exact sum on its two data classes
+EXACT = [("float32", "sum_exact"), ("float64", "sum_exact")]
 
 if __name__ == "__main__":
     n = 1 << 28
-    for dtype, op in PAIRS:
+    wl_exact = sys.argv[2] if len(sys.argv) > 2 else "u01"    # u01: the fast path
+    for dtype, op in (EXACT if sys.argv[1:2] == ["exact"] else PAIRS):
         x = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
-        inputs.fill_device(x, inputs.default_workload(dtype, op), seed=1)
+        wl = wl_exact if op == "sum_exact" else inputs.default_workload(dtype, op)
+        inputs.fill_device(x, wl, seed=1)
         rd.reduce(x, op)
         torch.cuda.synchronize()
         del x

@@ -161,6 +161,28 @@ def do_ops(args):
     return rows
 
 
+def do_exact(args):
+    """RD_SUM_EXACT next to the plain and compensated sums, per workload:
+    the exact kernel's fast path (one TwoSum per element) vs its slow path."""
+    rows = []
+    for log2n in args.log2n:
+        n = 1 << log2n
+        for dtype in ("float32", "float64"):
+            for wl in ("u01", "normalish", "wide", "wide_full"):
+                x = make(n, dtype, wl)
+                o = torch.empty((), dtype=x.dtype, device="cuda")
+                for op in ("sum", "sum_compensated", "sum_exact"):
+                    _, info = rd.reduce_ex(x, op, out=o)
+                    r = time_launch(lambda: rd.reduce(x, op, out=o), n * SIZE[dtype])
+                    r.update({"dtype": dtype, "workload": wl, "op": op, "n": n, "grid": info["grid"],
+                              "regs": info["regs_per_thread"], "ctas_per_sm": info["ctas_per_sm"],
+                              "variant": info["variant"]})
+                    rows.append(r)
+                    print(json.dumps(r), flush=True)
+                del x
+    return rows
+
+
 def do_sizes(args):
     rows = []
     for dtype in ("float32", "int32"):
@@ -333,14 +355,15 @@ def do_overhead(args):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi", "overhead"])
+    p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi", "overhead",
+                                    "exact"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
     args = p.parse_args()
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
            "grids": do_grids, "crossover": do_crossover, "multi": do_multi,
-           "overhead": do_overhead}[args.what](args)
+           "overhead": do_overhead, "exact": do_exact}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
         json.dump({"meta": meta, "result": res}, f, indent=1)
