@@ -151,6 +151,38 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
   return x ? (uint64_t)x : dflt;
 }
 
+// Bulk chunk schedule, fixed by the body size and the stage size only
+// (determinism): a head region in chunks of C0 (about 16 per SM, at most
+// 5000), then a tail region of 148*16 chunks of C1 = one stage, so the
+// dynamic schedule ends with short chunks and the per-SM tail imbalance is
+// < one C1 chunk. (16/16/1 measured best of a sweep, tools/tune_bulk.sh:
+// +0.9% over 12/4/2.)
+struct BulkPlan {
+  uint64_t c0, c1, head_region;
+  uint32_t nhead, nchunks;
+};
+bool plan_bulk(uint64_t body_bytes, uint64_t stage_bytes, BulkPlan* p) {
+  static const uint64_t kHeadPerSm = env_u64("RD_TUNE_HEAD_PER_SM", 16);
+  static const uint64_t kTailPerSm = env_u64("RD_TUNE_TAIL_PER_SM", 16);
+  static const uint64_t kTailStages = env_u64("RD_TUNE_TAIL_STAGES", 1);
+  const uint64_t T = body_bytes;
+  const uint64_t S = stage_bytes;
+  const uint64_t C1 = kTailStages * S;
+  const uint64_t R = T < 148ull * kTailPerSm * C1 ? T : 148ull * kTailPerSm * C1;
+  uint64_t c0 = T / (148ull * kHeadPerSm);
+  if (c0 < T / 5000) c0 = T / 5000;   // head <= 5000 chunks: head + tail <= kMaxSlots
+  c0 = (c0 + S - 1) / S * S;
+  if (c0 < 4 * S) c0 = 4 * S;
+  const uint64_t nhead = (T - R + c0 - 1) / c0;       // the head region is T - R bytes exactly
+  const uint64_t ntail = (R + C1 - 1) / C1;           // <= 148 * kTailPerSm
+  p->c0 = c0;
+  p->c1 = C1;
+  p->head_region = T - R;
+  p->nhead = (uint32_t)nhead;
+  p->nchunks = (uint32_t)(nhead + ntail);
+  return p->nchunks <= (uint32_t)kMaxSlots;
+}
+
 }  // namespace
 
 // Load (and configure) every default kernel now. With CUDA lazy loading, the
@@ -258,30 +290,16 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     a.tail = 0;
   }
   if (k.variant == RD_VARIANT_BULK) {
-    // Chunk schedule, fixed by n and the base alignment only (determinism):
-    // a head region in chunks of C0 (about 16 per SM, at most 5000), then a
-    // tail region of 148*16 chunks of C1 = one stage, so the dynamic schedule
-    // ends with short chunks and the per-SM tail imbalance is < one C1 chunk.
-    // (16/16/1 measured best of a sweep, tools/tune_bulk.sh: +0.9% over 12/4/2.)
-    static const uint64_t kHeadPerSm = env_u64("RD_TUNE_HEAD_PER_SM", 16);
-    static const uint64_t kTailPerSm = env_u64("RD_TUNE_TAIL_PER_SM", 16);
-    static const uint64_t kTailStages = env_u64("RD_TUNE_TAIL_STAGES", 1);
-    const uint64_t T = a.nvec * 16;
-    const uint64_t S = (uint64_t)k.vec_bytes;
-    const uint64_t C1 = kTailStages * S;
-    const uint64_t R = T < 148ull * kTailPerSm * C1 ? T : 148ull * kTailPerSm * C1;
-    uint64_t c0 = T / (148ull * kHeadPerSm);
-    if (c0 < T / 5000) c0 = T / 5000;   // head <= 5000 chunks: head + tail <= kMaxSlots
-    c0 = (c0 + S - 1) / S * S;
-    if (c0 < 4 * S) c0 = 4 * S;
-    const uint64_t nhead = (T - R + c0 - 1) / c0;       // the head region is T - R bytes exactly
-    const uint64_t ntail = (R + C1 - 1) / C1;           // <= 148 * kTailPerSm
-    a.chunk_bytes = c0;
-    a.tail_chunk_bytes = C1;
-    a.head_region_bytes = T - R;
-    a.nhead_chunks = (uint32_t)nhead;
-    a.nchunks = (uint32_t)(nhead + ntail);
-    if (a.nchunks > (uint32_t)kMaxSlots) { set_error("chunk schedule exceeds the workspace"); return RD_ERR_INVALID_ARG; }
+    BulkPlan bp;
+    if (!plan_bulk(a.nvec * 16, (uint64_t)k.vec_bytes, &bp)) {
+      set_error("chunk schedule exceeds the workspace");
+      return RD_ERR_INVALID_ARG;
+    }
+    a.chunk_bytes = bp.c0;
+    a.tail_chunk_bytes = bp.c1;
+    a.head_region_bytes = bp.head_region;
+    a.nhead_chunks = bp.nhead;
+    a.nchunks = bp.nchunks;
     a.work = ws.work;
     uint64_t need = a.nchunks ? a.nchunks : 1;
     if (g > need) g = need;
@@ -360,12 +378,18 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   if (mode == 0 && (uintptr_t)out % s != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
   if (mode == 1 && (uintptr_t)xrec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
+  int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
+  if (variant != RD_VARIANT_AUTO && variant != RD_VARIANT_VECTOR && variant != RD_VARIANT_BULK) {
+    set_error("RD_SUM_EXACT: variant must be auto, vector or bulk");
+    return RD_ERR_UNSUPPORTED;
+  }
+  if (variant == RD_VARIANT_AUTO) variant = (uint64_t)n * s >= kBulkMinBytes ? RD_VARIANT_BULK : RD_VARIANT_VECTOR;
   ExactRef k;
-  if (!lookup_exact(dtype, &k)) { set_error("no compiled exact-sum kernel (RD_TUNE_EXACT?)"); return RD_ERR_UNSUPPORTED; }
-  if (cfg && ((cfg->variant != RD_VARIANT_AUTO && cfg->variant != RD_VARIANT_VECTOR) ||
-              (cfg->unroll && cfg->unroll != k.unroll) || (cfg->vec_bytes && cfg->vec_bytes != k.vec_bytes) ||
+  if (!lookup_exact(dtype, variant, &k)) { set_error("no compiled exact-sum kernel (RD_TUNE_EXACT?)"); return RD_ERR_UNSUPPORTED; }
+  if (cfg && ((cfg->unroll && cfg->unroll != k.unroll) || (cfg->vec_bytes && cfg->vec_bytes != k.vec_bytes) ||
               (cfg->block && cfg->block != k.block))) {
-    set_error("RD_SUM_EXACT has one compiled configuration (vector loads, 32 B, U=6, 256 threads)");
+    set_error("RD_SUM_EXACT: one compiled configuration per variant (vector: 32 B loads, U=6, 256 threads; "
+              "bulk: the default ring)");
     return RD_ERR_UNSUPPORTED;
   }
   if (cfg && cfg->grid < 0) { set_error("bad rd_config"); return RD_ERR_INVALID_ARG; }
@@ -376,7 +400,7 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   DeviceInfo di;
   if ((st = device_info(dev, &di)) != RD_OK) return st;
   int occ = 1, regs = 0;
-  KernelRef kr{(ReduceFn)k.fn, k.block, k.unroll, k.vec_bytes, RD_VARIANT_VECTOR};
+  KernelRef kr{(ReduceFn)k.fn, k.block, k.unroll, k.vec_bytes, k.variant, k.smem_bytes};
   if ((st = occupancy(dev, kr, &occ, &regs)) != RD_OK) return st;
   Workspace ws;
   if ((st = get_workspace(dev, stream, &ws)) != RD_OK) return st;
@@ -385,18 +409,32 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   std::memset(&a, 0, sizeof(a));
   a.x = (const unsigned char*)x;
   a.n = n;
-  const uint64_t L = (uint64_t)(k.vec_bytes / s);
-  const uint64_t mis = (uint64_t)((uintptr_t)x % (uintptr_t)k.vec_bytes);
-  uint64_t head = ((k.vec_bytes - mis) % k.vec_bytes) / s;
+  const int vb = k.variant == RD_VARIANT_BULK ? 16 : k.vec_bytes;   // body alignment
+  const uint64_t L = (uint64_t)(vb / s);
+  const uint64_t mis = (uint64_t)((uintptr_t)x % (uintptr_t)vb);
+  uint64_t head = ((vb - mis) % vb) / s;
   if (head > n) head = n;
   a.head = head;
   a.nvec = (n - head) / L;
   a.tail_start = head + a.nvec * L;
   a.tail = n - a.tail_start;
   uint64_t g = (uint64_t)di.sms * occ;
-  uint64_t need = (a.nvec + (uint64_t)k.block * k.unroll - 1) / ((uint64_t)k.block * k.unroll);
-  if (need < 1) need = 1;
-  if (g > need) g = need;
+  if (k.variant == RD_VARIANT_BULK) {
+    BulkPlan bp;
+    if (!plan_bulk(a.nvec * 16, (uint64_t)k.vec_bytes, &bp)) { set_error("chunk schedule exceeds the workspace"); return RD_ERR_INVALID_ARG; }
+    a.chunk_bytes = bp.c0;
+    a.tail_chunk_bytes = bp.c1;
+    a.head_region_bytes = bp.head_region;
+    a.nhead_chunks = bp.nhead;
+    a.nchunks = bp.nchunks;
+    a.work = ws.work;
+    const uint64_t need = a.nchunks ? a.nchunks : 1;
+    if (g > need) g = need;
+  } else {
+    uint64_t need = (a.nvec + (uint64_t)k.block * k.unroll - 1) / ((uint64_t)k.block * k.unroll);
+    if (need < 1) need = 1;
+    if (g > need) g = need;
+  }
   if (cfg && cfg->grid > 0) g = (uint64_t)cfg->grid;
   if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
   a.out = out;
@@ -410,6 +448,7 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   std::memset(&lc, 0, sizeof(lc));
   lc.gridDim = dim3((unsigned)g);
   lc.blockDim = dim3((unsigned)k.block);
+  lc.dynamicSmemBytes = (size_t)k.smem_bytes;
   lc.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -420,7 +459,7 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   if (e != cudaSuccess) return cuda_fail(e, "exact-sum kernel launch");
   if (info) {
     std::memset(info, 0, sizeof(*info));
-    info->variant = RD_VARIANT_VECTOR;
+    info->variant = k.variant;
     info->vec_bytes = k.vec_bytes;
     info->unroll = k.unroll;
     info->block = k.block;

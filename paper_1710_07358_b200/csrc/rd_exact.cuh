@@ -34,7 +34,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "rd_kernels.cuh"
+#include "rd_bulk.cuh"
 
 namespace rd {
 
@@ -69,6 +69,11 @@ struct XArgs {
   unsigned* ticket;
   uint32_t tag;
   int mode;
+  // bulk variant only: the chunk schedule (as KArgs; the exact sum does not
+  // depend on which CTA takes which chunk, so no per-chunk partials)
+  uint64_t chunk_bytes, tail_chunk_bytes, head_region_bytes;
+  uint32_t nchunks, nhead_chunks;
+  unsigned* work;
 };
 
 // ------------------------------------------------------------ superaccumulator
@@ -217,10 +222,13 @@ __device__ __forceinline__ bool spec2(Ex (&ex)[E], const double (&xs)[L]) {
 #pragma unroll
   for (int l = 0; l < L; ++l) {
     Ex& q = ex[l % E];
-    double s, e, s1, e1;
+    double s, e;
     two_sum(q.a0, xs[l], s, e);
-    two_sum(q.a1, e, s1, e1);
-    bad |= !(e1 == 0.0 && fabs(s1) <= 1.7976931348623157e308);   // NaN for inf/NaN/overflow
+    // a1 + e exact? the symmetric difference test (see fold_vec_exact): 3 DADD
+    // + 2 compares instead of a second TwoSum; NaN (inf/NaN term, overflow)
+    // fails a compare
+    const double s1 = __dadd_rn(q.a1, e);
+    bad |= (__dsub_rn(s1, q.a1) != e) | (__dsub_rn(s1, e) != q.a1);
     q.a0 = s;
     q.a1 = s1;
   }
@@ -247,12 +255,19 @@ __device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L
   for (int j = 0; j < E; ++j) save[j] = ex[j];
   bool bad = false;
   if constexpr (sizeof(T) == 4) {
+    // fp32 terms: speculate that every add into a0 is exact, tested without
+    // TwoSum's error term: s == a0 + x exactly iff fl(s - a0) == x and
+    // fl(s - x) == a0. (If s is inexact, the difference taken from the
+    // operand of larger magnitude is exact -- Dekker's Fast2Sum lemma -- and
+    // differs from the other operand by the nonzero rounding error; if s is
+    // exact both differences are.) 3 DADD + 2 compares per element instead of
+    // 6 + 1: the FP64 pipe is the limiter. inf/NaN terms and overflow fail a
+    // compare (inf - inf, NaN).
 #pragma unroll
-    for (int l = 0; l < L; ++l) {                // one TwoSum per element, speculating e == 0
+    for (int l = 0; l < L; ++l) {
       Ex& q = ex[l % E];
-      double s, e;
-      two_sum(q.a0, xs[l], s, e);
-      bad |= (e != 0.0);                         // NaN (inf/NaN term) counts as failed
+      const double s = __dadd_rn(q.a0, xs[l]);
+      bad |= (__dsub_rn(s, q.a0) != xs[l]) | (__dsub_rn(s, xs[l]) != q.a0);
       q.a0 = s;
     }
     if (__builtin_expect(!bad, 1)) return;
@@ -326,65 +341,16 @@ __device__ __forceinline__ void exact_store(const long long* w, uint32_t flags, 
   else *(uint64_t*)out = b;
 }
 
-// --------------------------------------------------------------------- kernel
-template <typename T, int B, int U, int E, int MINB>
-__global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
-  using TR = ExactTraits<T>;
-  constexpr int NW = TR::kWords;
-  constexpr int VB = 32;
-  constexpr int L = VB / (int)sizeof(T);
+// a3-a7, shared by both exact kernels: expansions -> warp superaccumulators
+// -> the CTA's slot -> (last CTA) the sum of the G slots, rounded once.
+template <typename T, int B, int E>
+__device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
+                                             long long* tot, unsigned& s_flags, unsigned& s_last,
+                                             const XArgs& args) {
+  constexpr int NW = ExactTraits<T>::kWords;
   constexpr int NWARP = B / 32;
-  __shared__ long long sacc[NWARP][NW];
-  __shared__ long long tot[B];
-  __shared__ unsigned s_flags, s_last;
-
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
-  if (threadIdx.x == 0) s_flags = 0;
-  __syncthreads();
   long long* w = sacc[warp];
-
-  Ex ex[E];
-#pragma unroll
-  for (int j = 0; j < E; ++j) ex[j] = Ex{-0.0, -0.0, -0.0};
-  uint32_t flags = 0;
-
-  const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * B;
-  const unsigned char* body = args.x + args.head * sizeof(T);
-  pdl_wait();
-  const uint64_t nvec = args.nvec;
-  uint64_t i = tid;
-  // The main loop's trip count is warp-uniform (tested on the warp's last
-  // lane, whose index is the largest), so every iteration can end with a
-  // __syncwarp: a lane that replayed a vector (divergent) rejoins its warp
-  // there. Without it the warp stayed split after the first divergent replay
-  // and ran the loop ~2 lanes at a time (ncu: 2.0 avg threads per F2F).
-  const uint64_t lag = 31 - (uint64_t)ln;        // lane 31's index = i + lag
-  for (; i + lag + (uint64_t)(U - 1) * stride < nvec; i += (uint64_t)U * stride) {
-    Vec<VB> v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      double xs[L];
-#pragma unroll
-      for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v[u], l));
-      fold_vec_exact<T, E, L>(ex, xs, w, flags);
-    }
-    __syncwarp();
-  }
-  for (; i < nvec; i += stride) {
-    Vec<VB> v = ldg_stream<VB>(body + i * VB);
-    double xs[L];
-#pragma unroll
-    for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v, l));
-    fold_vec_exact<T, E, L>(ex, xs, w, flags);
-  }
-  pdl_trigger();
-  // a2: head and tail stragglers
-  if (tid < args.head) ex_add<T>(ex[0], widen(ldg_scalar<T>(args.x + tid * sizeof(T))), w, flags);
-  if (tid < args.tail) ex_add<T>(ex[1], widen(ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T))), w, flags);
   // a3: the expansions into the warp's superaccumulator. Every term passes
   // through some a0 (or the slow path, which flags itself), and an a0 that
   // has seen a term other than -0.0 is never -0.0 again (x + -x = +0), so a0
@@ -447,6 +413,7 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
   if (threadIdx.x == 0) {
     sacc_normalise<NW>(sacc[0]);
     *args.ticket = 0u;
+    if (args.work) *args.work = 0u;
     if (args.mode == 0) {
       exact_store<T>(sacc[0], s_flags, args.n, args.out);
     } else {
@@ -461,6 +428,192 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
       for (int k = NW; k < RD_EXACT_MAX_WORDS; ++k) r->word[k] = 0;
     }
   }
+}
+
+// --------------------------------------------------------------------- kernel
+template <typename T, int B, int U, int E, int MINB>
+__global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
+  using TR = ExactTraits<T>;
+  constexpr int NW = TR::kWords;
+  constexpr int VB = 32;
+  constexpr int L = VB / (int)sizeof(T);
+  constexpr int NWARP = B / 32;
+  __shared__ long long sacc[NWARP][NW];
+  __shared__ long long tot[B];
+  __shared__ unsigned s_flags, s_last;
+
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_flags = 0;
+  __syncthreads();
+  long long* w = sacc[warp];
+
+  Ex ex[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) ex[j] = Ex{-0.0, -0.0, -0.0};
+  uint32_t flags = 0;
+
+  const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * B;
+  const unsigned char* body = args.x + args.head * sizeof(T);
+  pdl_wait();
+  const uint64_t nvec = args.nvec;
+  uint64_t i = tid;
+  // The main loop's trip count is warp-uniform (tested on the warp's last
+  // lane, whose index is the largest), so every iteration can end with a
+  // __syncwarp: a lane that replayed a vector (divergent) rejoins its warp
+  // there. Without it the warp stayed split after the first divergent replay
+  // and ran the loop ~2 lanes at a time (ncu: 2.0 avg threads per F2F).
+  const uint64_t lag = 31 - (uint64_t)ln;        // lane 31's index = i + lag
+  for (; i + lag + (uint64_t)(U - 1) * stride < nvec; i += (uint64_t)U * stride) {
+    Vec<VB> v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double xs[L];
+#pragma unroll
+      for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v[u], l));
+      fold_vec_exact<T, E, L>(ex, xs, w, flags);
+    }
+    __syncwarp();
+  }
+  for (; i < nvec; i += stride) {
+    Vec<VB> v = ldg_stream<VB>(body + i * VB);
+    double xs[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v, l));
+    fold_vec_exact<T, E, L>(ex, xs, w, flags);
+  }
+  pdl_trigger();
+  // a2: head and tail stragglers
+  if (tid < args.head) ex_add<T>(ex[0], widen(ldg_scalar<T>(args.x + tid * sizeof(T))), w, flags);
+  if (tid < args.tail) ex_add<T>(ex[1], widen(ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T))), w, flags);
+  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
+}
+
+// The bulk-copy form (like rd_bulk_kernel): one producer lane streams
+// chunks (static first chunk, then a global counter) into a STAGES-deep
+// shared-memory ring with cp.async.bulk; CW consumer warps LDS.128 their
+// slice of each stage into fold_vec_exact. Memory parallelism comes from the
+// ring (STAGES * STAGE_BYTES in flight per SM), not from registers -- the
+// vector kernel's 118 registers/thread cap it at 16 warps/SM.
+template <typename T, int STAGES, int STAGE_BYTES, int CW, int E>
+__global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const XArgs args) {
+  using TR = ExactTraits<T>;
+  constexpr int NW = TR::kWords;
+  constexpr int B = 32 * (CW + 1);
+  constexpr int CT = 32 * CW;
+  constexpr int L = 16 / (int)sizeof(T);
+  constexpr int PER_THREAD = STAGE_BYTES / (16 * CT);
+  static_assert(STAGE_BYTES % (16 * CT) == 0, "stage must split evenly over consumer threads");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* ring = smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint32_t* st_bytes = reinterpret_cast<uint32_t*>(empty + STAGES);   // 0 = no more chunks
+  __shared__ long long sacc[B / 32][NW];
+  __shared__ long long tot[B];
+  __shared__ unsigned s_flags, s_last;
+
+  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < (B / 32) * NW; i += B) (&sacc[0][0])[i] = 0;
+  if (threadIdx.x == 0) {
+    s_flags = 0;
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  Ex ex[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) ex[j] = Ex{-0.0, -0.0, -0.0};
+  uint32_t flags = 0;
+  const unsigned char* body = args.x + args.head * sizeof(T);
+  const uint64_t body_bytes = args.nvec * 16;
+  pdl_wait();
+  if (warp == CW) {
+    if (ln == 0) {                                   // producer
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t c = blockIdx.x;
+      uint32_t next = atomicAdd(args.work, 1u) + gridDim.x;
+      for (;; c = next, next = atomicAdd(args.work, 1u) + gridDim.x) {
+        if (c >= args.nchunks) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          st_bytes[stage] = 0;
+          mbar_arrive(&full[stage]);
+          break;
+        }
+        uint64_t cbeg, clen;
+        chunk_range(args, c, body_bytes, &cbeg, &clen);
+        const uint64_t cend = cbeg + clen;
+        for (uint64_t off = cbeg; off < cend; off += STAGE_BYTES) {
+          const uint32_t bytes = (uint32_t)min((uint64_t)STAGE_BYTES, cend - off);
+          mbar_wait(&empty[stage], phase ^ 1);
+          st_bytes[stage] = bytes;
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(ring + (size_t)stage * STAGE_BYTES, body + off, bytes, &full[stage], pol);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {                                           // consumers
+    long long* w = sacc[warp];
+    const int t = threadIdx.x;
+    const uint32_t ring_addr = smem_addr(ring);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      mbar_wait(&full[stage], phase);
+      const uint32_t bytes = st_bytes[stage];
+      if (bytes == 0) break;
+      const uint32_t base = ring_addr + stage * STAGE_BYTES;
+      if (bytes == STAGE_BYTES) {
+        uint4 v[PER_THREAD];
+#pragma unroll
+        for (int k = 0; k < PER_THREAD; ++k) v[k] = lds128(base + (k * CT + t) * 16);
+#pragma unroll
+        for (int k = 0; k < PER_THREAD; ++k) {
+          Vec<16> q{{v[k].x, v[k].y, v[k].z, v[k].w}};
+          double xs[L];
+#pragma unroll
+          for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, 16>(q, l));
+          fold_vec_exact<T, E, L>(ex, xs, w, flags);
+        }
+      } else {
+        for (int k = 0; k < PER_THREAD; ++k) {
+          const uint32_t off = (k * CT + t) * 16;
+          if (off < bytes) {
+            const uint4 r = lds128(base + off);
+            Vec<16> q{{r.x, r.y, r.z, r.w}};
+            double xs[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, 16>(q, l));
+            fold_vec_exact<T, E, L>(ex, xs, w, flags);
+          }
+        }
+      }
+      // reconverge (a replayed vector diverges), then release the stage
+      __syncwarp();
+      if (ln == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&empty[stage]);
+      }
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+    // a2: head and tail stragglers (< 16 bytes each), CTA 0's first threads
+    if (blockIdx.x == 0) {
+      if ((uint64_t)t < args.head) ex_add<T>(ex[0], widen(ldg_scalar<T>(args.x + t * sizeof(T))), w, flags);
+      if ((uint64_t)t < args.tail)
+        ex_add<T>(ex[E - 1], widen(ldg_scalar<T>(args.x + (args.tail_start + t) * sizeof(T))), w, flags);
+    }
+  }
+  pdl_trigger();
+  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
 }
 
 // Fold `count` exact records (any order gives the same integer): one CTA.

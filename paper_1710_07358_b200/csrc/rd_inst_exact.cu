@@ -18,12 +18,25 @@ static bool pick(int u, int e, int m, ExactRef* r) {
     *r = ExactRef{rd_exact_kernel<T, kBlock, U, E, M>, kBlock, U, 32};                            \
     return true;                                                                                   \
   }
-  RD_X(6, 2, 1) RD_X(4, 2, 1) RD_X(8, 1, 1) RD_X(6, 1, 1) RD_X(2, 2, 3)
+  RD_X(6, 2, 2) RD_X(6, 2, 1) RD_X(4, 2, 2) RD_X(8, 1, 2) RD_X(2, 2, 3)
 #undef RD_X
   return false;
 }
 
-bool lookup_exact(int dtype, ExactRef* r) {
+template <typename T>
+static bool pick_bulk(ExactRef* r) {
+  constexpr int CW = kExactBulkConsumerWarps;
+  *r = ExactRef{rd_exact_bulk_kernel<T, kBulkStages, kBulkStageBytes, CW, kExactExpansions>, 32 * (CW + 1),
+                kBulkStages, kBulkStageBytes, RD_VARIANT_BULK, BulkSmem<kBulkStages, kBulkStageBytes, CW>::kBytes};
+  return true;
+}
+
+bool lookup_exact(int dtype, int variant, ExactRef* r) {
+  if (variant == RD_VARIANT_BULK) {
+    if (dtype == RD_FLOAT32) return pick_bulk<float>(r);
+    if (dtype == RD_FLOAT64) return pick_bulk<double>(r);
+    return false;
+  }
   static int tu = 0, te = 0, tm = 0;
   static bool once = [] {
     const char* v = std::getenv("RD_TUNE_EXACT");

@@ -78,8 +78,9 @@ struct KArgs {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// chunk c of the bulk schedule -> [off, off + len) of the body
-__device__ __forceinline__ void chunk_range(const struct KArgs& a, uint32_t c, uint64_t body_bytes,
+// chunk c of the bulk schedule -> [off, off + len) of the body (A: KArgs or XArgs)
+template <class A>
+__device__ __forceinline__ void chunk_range(const A& a, uint32_t c, uint64_t body_bytes,
                                             uint64_t* off, uint64_t* len) {
   if (c < a.nhead_chunks) {
     *off = (uint64_t)c * a.chunk_bytes;

@@ -36,11 +36,14 @@ using ExactCombineFn = void (*)(const rd_exact_record*, int, uint32_t, void*, rd
 struct ExactRef {
   ExactFn fn;
   int block, unroll, vec_bytes;
+  int variant = RD_VARIANT_VECTOR;   // or RD_VARIANT_BULK (unroll = stages, vec_bytes = stage bytes)
+  int smem_bytes = 0;
 };
 constexpr int kExactUnroll = 6;       // 32-byte loads in flight per thread per iteration (tools/tune_exact.py)
 constexpr int kExactExpansions = 2;   // independent (a0, a1) expansions per thread
-constexpr int kExactMinBlocks = 1;    // __launch_bounds__ min CTAs/SM (register cap)
-bool lookup_exact(int dtype, ExactRef* r);
+constexpr int kExactMinBlocks = 2;    // __launch_bounds__ min CTAs/SM (register cap: <= 128)
+constexpr int kExactBulkConsumerWarps = 16;   // bulk variant: the fold is FP64-latency bound
+bool lookup_exact(int dtype, int variant, ExactRef* r);
 ExactCombineFn lookup_exact_combine(int dtype);
 
 // bulk variant: CW consumer warps + 1 producer warp per CTA. 8 consumer warps

@@ -56,10 +56,12 @@ def test_exact_offsets_grids_and_shards(rd, dtype):
     for off in range(8):
         xd = to_dev(x, off)
         assert same(val(rd.reduce(xd, "sum_exact")), want), off
+        assert same(val(rd.reduce_ex(xd, "sum_exact", variant="bulk")[0]), want), off
     xd = to_dev(x, 3)
-    for grid in (1, 2, 3, 7, 148, 296, 1000, 4096):
-        got, info = rd.reduce_ex(xd, "sum_exact", grid=grid)
-        assert info["grid"] == grid and same(val(got), want), grid
+    for variant in ("vector", "bulk"):
+        for grid in (1, 2, 3, 7, 148, 296, 1000, 4096):
+            got, info = rd.reduce_ex(xd, "sum_exact", variant=variant, grid=grid)
+            assert info["grid"] == grid and info["variant"] == variant and same(val(got), want), (variant, grid)
     RB = rd.EXACT_RECORD_BYTES
     for W in (1, 2, 3, 8, 17):
         recs = torch.empty(W * RB, dtype=torch.uint8, device="cuda")
@@ -141,7 +143,9 @@ def test_exact_full_size(rd, dtype, wl):
     for r in range(8):
         b, c = rd.shard_range(n, 8, r)
         rd.reduce_exact_partial(x[b:b + c], rec=recs[r * RB:(r + 1) * RB])
-    alt = {bits(val(rd.combine_exact_records(recs, dtype))), bits(val(rd.reduce_ex(x, "sum_exact", grid=999)[0]))}
+    alt = {bits(val(rd.combine_exact_records(recs, dtype))), bits(val(rd.reduce_ex(x, "sum_exact", grid=999)[0])),
+           bits(val(rd.reduce_ex(x, "sum_exact", variant="vector")[0])),
+           bits(val(rd.reduce_ex(x, "sum_exact", variant="bulk", grid=37)[0]))}
     xh = x.cpu().numpy()
     del x
     want = oracle.reduce(xh, "sum_exact").value

@@ -171,9 +171,10 @@ def do_exact(args):
             for wl in ("u01", "normalish", "wide", "wide_full"):
                 x = make(n, dtype, wl)
                 o = torch.empty((), dtype=x.dtype, device="cuda")
-                for op in ("sum", "sum_compensated", "sum_exact"):
-                    _, info = rd.reduce_ex(x, op, out=o)
-                    r = time_launch(lambda: rd.reduce(x, op, out=o), n * SIZE[dtype])
+                for op, var in (("sum", "auto"), ("sum_compensated", "auto"), ("sum_exact", "vector"),
+                                ("sum_exact", "bulk")):
+                    _, info = rd.reduce_ex(x, op, variant=var, out=o)
+                    r = time_launch(lambda: rd.reduce_ex(x, op, variant=var, out=o), n * SIZE[dtype])
                     r.update({"dtype": dtype, "workload": wl, "op": op, "n": n, "grid": info["grid"],
                               "regs": info["regs_per_thread"], "ctas_per_sm": info["ctas_per_sm"],
                               "variant": info["variant"]})
