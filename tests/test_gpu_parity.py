@@ -19,7 +19,7 @@ INT = ["int32", "uint32", "int64"]
 FLT = ["float32", "float64"]
 INT_OPS = ["sum", "prod", "min", "max", "and", "or", "xor"]
 FLT_OPS = ["sum", "prod", "min", "max"]
-EXTRA_OPS = ["argmin", "argmax", "sum_compensated"]
+EXTRA_OPS = ["argmin", "argmax", "sum_compensated", "sum_exact"]
 PAIRS = [(d, o) for d in INT for o in INT_OPS + EXTRA_OPS] + [(d, o) for d in FLT for o in FLT_OPS + EXTRA_OPS]
 SIZES = [0, 1, 2, 3, 7, 8, 9, 31, 32, 33, 255, 256, 257, 1023, 1025, 4097, 65535, 65537,
          (1 << 20) + 1, 5533214]
@@ -645,6 +645,19 @@ def test_c5_full_size_2_34(rd):
             ref = _oracle_stream(x, "sum")
             _parity.check(whole, np.zeros(0, np.float32), "sum", ref=ref)
             _parity.check(sharded, np.zeros(0, np.float32), "sum", ref=ref)
+            # the exact sum (reading R17): one result for the whole array, the
+            # 8-shard exact records and another grid (bit-exact parity with the
+            # exact oracle is checked at 2^28; streaming it over 2^34 terms
+            # would take ~10 min), inside the plain sum's 4 eps sum|x| bound
+            RB = rd.EXACT_RECORD_BYTES
+            xrecs = torch.empty(8 * RB, dtype=torch.uint8, device="cuda")
+            for r in range(8):
+                b, c = rd.shard_range(n, 8, r)
+                rd.reduce_exact_partial(x[b:b + c], rec=xrecs[r * RB:(r + 1) * RB])
+            ex = {val(rd.reduce(x, "sum_exact")).tobytes(), val(rd.combine_exact_records(xrecs, "float32")).tobytes(),
+                  val(rd.reduce_ex(x, "sum_exact", grid=777)[0]).tobytes()}
+            assert len(ex) == 1
+            _parity.check(np.frombuffer(ex.pop(), np.float32)[0], np.zeros(0, np.float32), "sum", ref=ref)
     del x
 
 

@@ -33,8 +33,8 @@ import paper_1710_07358_b200 as rd  # noqa: E402
 from tests import _parity  # noqa: E402
 
 SIZE = {"int32": 4, "uint32": 4, "int64": 8, "float32": 4, "float64": 8}
-INT_OPS = ["sum", "prod", "min", "max", "and", "or", "xor", "argmin", "argmax", "sum_compensated"]
-FLT_OPS = ["sum", "prod", "min", "max", "argmin", "argmax", "sum_compensated"]
+INT_OPS = ["sum", "prod", "min", "max", "and", "or", "xor", "argmin", "argmax", "sum_compensated", "sum_exact"]
+FLT_OPS = ["sum", "prod", "min", "max", "argmin", "argmax", "sum_compensated", "sum_exact"]
 L2 = 126 * 2 ** 20
 
 

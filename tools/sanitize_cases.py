@@ -6,7 +6,7 @@ synccheck, initcheck) runs on one GPU:
 
 Covers both kernel variants (vector, bulk), the paper-listing variant, every
 (dtype, op) pair, misaligned bases, forced multi-CTA grids (ticket path), arg
-ops, records + rd_combine_records, and reduce_host. Exits non-zero if a result
+ops, records + rd_combine_records, exact records, and reduce_host. Exits non-zero if a result
 disagrees with the oracle."""
 import os
 import sys
@@ -21,8 +21,8 @@ import inputs  # noqa: E402
 import paper_1710_07358_b200 as rd  # noqa: E402
 from tests import _parity  # noqa: E402
 
-INT_OPS = ["sum", "prod", "min", "max", "and", "or", "xor", "argmin", "argmax", "sum_compensated"]
-FLT_OPS = ["sum", "prod", "min", "max", "argmin", "argmax", "sum_compensated"]
+INT_OPS = ["sum", "prod", "min", "max", "and", "or", "xor", "argmin", "argmax", "sum_compensated", "sum_exact"]
+FLT_OPS = ["sum", "prod", "min", "max", "argmin", "argmax", "sum_compensated", "sum_exact"]
 
 
 def dev(x, off=0):
@@ -64,6 +64,14 @@ def main():
             b, c = rd.shard_range(x.size, 4, r)
             rd.reduce_partial(xd[b:b + c], op, rec=recs[r * 32:(r + 1) * 32])
         _parity.check(val(rd.combine_records(recs, "float32", op)), x, op)
+    RB = rd.EXACT_RECORD_BYTES
+    xrecs = torch.zeros(4 * RB, dtype=torch.uint8, device="cuda")
+    for r in range(4):
+        b, c = rd.shard_range(x.size, 4, r)
+        rd.reduce_exact_partial(xd[b:b + c], rec=xrecs[r * RB:(r + 1) * RB])
+    _parity.check(val(rd.combine_exact_records(xrecs, "float32")), x, "sum_exact")
+    w = inputs.generate(50001, "float64", "wide_full", seed=4)
+    _parity.check(val(rd.reduce(dev(w, 1), "sum_exact")), w, "sum_exact")
     big = inputs.generate((1 << 23) + 5, "float64", "u01", seed=2)
     _parity.check(rd.reduce_host(big, "sum"), big, "sum")
     torch.cuda.synchronize()

@@ -144,7 +144,7 @@ def do_ops(args):
     rows = []
     pairs = [(d, o) for d in ("int32", "uint32", "int64") for o in rd.OPS] + \
             [(d, o) for d in ("float32", "float64")
-             for o in ("sum", "prod", "min", "max", "argmin", "argmax", "sum_compensated")]
+             for o in ("sum", "prod", "min", "max", "argmin", "argmax", "sum_compensated", "sum_exact")]
     for log2n in args.log2n:
         n = 1 << log2n
         for dtype, op in pairs:
