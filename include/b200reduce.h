@@ -83,10 +83,11 @@ typedef enum {
    * that sum, so the bits do not depend on the grid, variant, base alignment
    * or number of GPUs. Any NaN, or +inf with -inf -> NaN; else +-inf if any;
    * a finite exact sum past the dtype's range -> +-inf; an exact zero is -0.0
-   * iff every term is -0.0. Floats: reduce, reduce_multi, reduce_host and
-   * reduce_exact_partial / rd_combine_exact_records (the 32-byte rd_record
-   * cannot carry an exact partial, so reduce_partial, rd_combine_records and
-   * reduce_fused return RD_ERR_UNSUPPORTED for float dtypes).
+   * iff every term is -0.0. Floats: reduce, rd_reduce_ex (vector / bulk),
+   * reduce_multi, reduce_fused, reduce_host and reduce_exact_partial /
+   * rd_combine_exact_records (the 32-byte rd_record cannot carry an exact
+   * partial, so reduce_partial and rd_combine_records return
+   * RD_ERR_UNSUPPORTED for float dtypes).
    * Integers: identical to RD_SUM everywhere. */
   RD_SUM_EXACT = 10
 } rd_op;

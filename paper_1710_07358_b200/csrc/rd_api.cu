@@ -192,6 +192,16 @@ bool plan_bulk(uint64_t body_bytes, uint64_t stage_bytes, BulkPlan* p) {
 // communicator is connected.
 rd_status preload_default_kernels(int dev) {
   for (int dt = RD_INT32; dt <= RD_FLOAT64; ++dt) {
+    if (dt == RD_FLOAT32 || dt == RD_FLOAT64) {     // the exact-sum kernels (fused mode 2 too)
+      for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK}) {
+        ExactRef x;
+        if (!lookup_exact(dt, variant, &x)) continue;
+        int occ = 0, regs = 0;
+        rd_status st = occupancy(dev, KernelRef{(ReduceFn)x.fn, x.block, x.unroll, x.vec_bytes, x.variant, x.smem_bytes},
+                                 &occ, &regs);
+        if (st != RD_OK) return st;
+      }
+    }
     for (int op = RD_SUM; op <= RD_SUM_EXACT; ++op) {
       if (check_dtype_op(dt, op) != RD_OK) continue;
       for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK}) {
@@ -229,12 +239,12 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   if (mode == 1 && (uintptr_t)rec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
   if (is_exact_float(dtype, op)) {
-    if (mode != 0) {
+    if (mode == 1) {
       set_error("RD_SUM_EXACT on floats: the 32-byte rd_record cannot carry an exact partial "
                 "(use reduce_exact_partial / reduce_multi)");
       return RD_ERR_UNSUPPORTED;
     }
-    return launch_exact(x, n, dtype, 0, out, nullptr, stream, cfg, info);
+    return launch_exact(x, n, dtype, mode, out, nullptr, stream, cfg, info, fused);
   }
 
   int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
@@ -365,17 +375,18 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
 // RD_SUM_EXACT on a float dtype (rd_exact.cuh): validate, plan, launch.
 // mode 0 writes one element to `out`, mode 1 one rd_exact_record to `xrec`.
 rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, rd_exact_record* xrec,
-                       cudaStream_t stream, const rd_config* cfg, rd_launch_info* info) {
+                       cudaStream_t stream, const rd_config* cfg, rd_launch_info* info, const FusedArgs* fused) {
   if (dtype != RD_FLOAT32 && dtype != RD_FLOAT64) {
     set_error("exact partials are for float dtypes (integer sums are exact: use reduce_partial)");
     return RD_ERR_UNSUPPORTED;
   }
   const int s = dtype_size(dtype);
   if (x == nullptr && n > 0) { set_error("x is NULL"); return RD_ERR_INVALID_ARG; }
-  if (mode == 0 && out == nullptr) { set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
+  if ((mode == 0 || mode == 2) && out == nullptr) { set_error("out is NULL"); return RD_ERR_INVALID_ARG; }
   if (mode == 1 && xrec == nullptr) { set_error("rec is NULL"); return RD_ERR_INVALID_ARG; }
+  if (mode == 2 && fused == nullptr) { set_error("fused args missing"); return RD_ERR_INVALID_ARG; }
   if ((uintptr_t)x % s != 0) { set_error("x is not aligned to sizeof(dtype)"); return RD_ERR_MISALIGNED; }
-  if (mode == 0 && (uintptr_t)out % s != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
+  if (mode != 1 && (uintptr_t)out % s != 0) { set_error("out is not aligned"); return RD_ERR_MISALIGNED; }
   if (mode == 1 && (uintptr_t)xrec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
   int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
@@ -443,6 +454,13 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   a.ticket = ws.ticket;
   a.tag = record_tag(dtype, RD_SUM_EXACT);
   a.mode = mode;
+  if (fused) {
+    a.peers = fused->peers;
+    a.self = fused->self;
+    a.err = fused->err;
+    a.nranks = fused->nranks;
+    a.rank = fused->rank;
+  }
 
   cudaLaunchConfig_t lc;
   std::memset(&lc, 0, sizeof(lc));

@@ -74,6 +74,11 @@ struct XArgs {
   uint64_t chunk_bytes, tail_chunk_bytes, head_region_bytes;
   uint32_t nchunks, nhead_chunks;
   unsigned* work;
+  // mode 2 (fused multi-GPU exchange, rd_kernels.cuh Mailbox) only
+  Mailbox* const* peers;
+  Mailbox* self;
+  int* err;
+  int nranks, rank;
 };
 
 // ------------------------------------------------------------ superaccumulator
@@ -341,6 +346,84 @@ __device__ __forceinline__ void exact_store(const long long* w, uint32_t flags, 
   else *(uint64_t*)out = b;
 }
 
+// The fused multi-GPU exchange of exact records (reduce_fused with
+// RD_SUM_EXACT; the LL protocol of rd_kernels.cuh fused_exchange, 4 + 2*NW
+// self-validating words per rank): warp 0 of the last CTA pushes this rank's
+// carried words into slot [epoch&1][rank] of every mailbox, polls its own
+// until the W records of this epoch are complete, adds them word by word
+// (integers: the same bits on every rank, whatever the arrival order), and
+// rounds once.
+template <typename T>
+__device__ __noinline__ void exact_fused_exchange(long long* words, unsigned flags, const XArgs& args) {
+  constexpr int NW = ExactTraits<T>::kWords;
+  constexpr int NP = 4 + 2 * NW;                     // payload words
+  static_assert(NP <= kExactLLWords, "mailbox too small");
+  const int ln = threadIdx.x & 31;
+  const unsigned long long epoch = *(volatile unsigned long long*)&args.self->epoch + 1;
+  const int par = (int)(epoch & 1);
+  const unsigned long long eflag = (unsigned long long)(uint32_t)epoch << 32;
+  const int W = args.nranks;
+  auto payload = [&](int k) -> uint32_t {
+    if (k == 0) return args.tag;
+    if (k == 1) return (uint32_t)args.n;
+    if (k == 2) return (uint32_t)(args.n >> 32);
+    if (k == 3) return flags;
+    const unsigned long long v = (unsigned long long)words[(k - 4) >> 1];
+    return (k & 1) ? (uint32_t)(v >> 32) : (uint32_t)v;
+  };
+  for (int p = 0; p < W; ++p) {
+    volatile unsigned long long* dst = args.peers[p]->xll[par][args.rank];
+    for (int k = ln; k < NP; k += 32) dst[k] = eflag | payload(k);   // peer stores over NVLink
+  }
+  bool timeout = false;
+  for (int q = 0; q < W && !timeout; ++q) {
+    const volatile unsigned long long* src = args.self->xll[par][q];
+    for (int k = ln; k < NP; k += 32) {
+      uint32_t spins = 0;
+      while ((src[k] & 0xffffffff00000000ull) != eflag) {
+        if (++spins > 4096) __nanosleep(128);
+        if (spins > (1u << 25)) { timeout = true; break; }
+      }
+      if (timeout) break;
+    }
+    timeout = __any_sync(0xffffffffu, timeout);
+  }
+  __syncwarp();
+  // every word of every record is in: sum them (lane j: words j, j+32, ...)
+  bool bad = false;
+  unsigned long long n = 0;
+  unsigned fl = 0;
+  if (!timeout) {
+    for (int q = 0; q < W; ++q) {
+      const volatile unsigned long long* src = args.self->xll[par][q];
+      bad |= (uint32_t)src[0] != args.tag;
+      n += ((unsigned long long)(uint32_t)src[2] << 32) | (uint32_t)src[1];
+      fl |= (uint32_t)src[3];
+    }
+    for (int j = ln; j < NW; j += 32) {
+      long long s = 0;
+      for (int q = 0; q < W; ++q) {
+        const volatile unsigned long long* src = args.self->xll[par][q];
+        s += (long long)((((unsigned long long)(uint32_t)src[5 + 2 * j]) << 32) | (uint32_t)src[4 + 2 * j]);
+      }
+      words[j] = s;                                  // < W * 2^32 per word
+    }
+  }
+  __syncwarp();
+  if (ln == 0) {
+    if (timeout) atomicExch(args.err, (int)RD_ERR_TIMEOUT);
+    else if (bad) atomicExch(args.err, (int)RD_ERR_MISMATCH);
+    if (timeout || bad || n == 0) {
+      if constexpr (sizeof(T) == 4) *(uint32_t*)args.out = 0u;
+      else *(uint64_t*)args.out = 0ull;
+    } else {
+      sacc_normalise<NW>(words);
+      exact_store<T>(words, fl, n, args.out);
+    }
+    *(volatile unsigned long long*)&args.self->epoch = epoch;
+  }
+}
+
 // a3-a7, shared by both exact kernels: expansions -> warp superaccumulators
 // -> the CTA's slot -> (last CTA) the sum of the G slots, rounded once.
 template <typename T, int B, int E>
@@ -416,7 +499,7 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
     if (args.work) *args.work = 0u;
     if (args.mode == 0) {
       exact_store<T>(sacc[0], s_flags, args.n, args.out);
-    } else {
+    } else if (args.mode == 1) {
       rd_exact_record* r = args.rec;
       r->tag = args.tag;
       r->status = 0;
@@ -427,6 +510,10 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
       for (int k = 0; k < NW; ++k) r->word[k] = sacc[0][k];
       for (int k = NW; k < RD_EXACT_MAX_WORDS; ++k) r->word[k] = 0;
     }
+  }
+  if (args.mode == 2 && threadIdx.x < 32) {
+    __syncwarp();
+    exact_fused_exchange<T>(sacc[0], s_flags, args);
   }
 }
 

@@ -23,12 +23,30 @@ static bool pick(int u, int e, int m, ExactRef* r) {
   return false;
 }
 
+template <typename T, int CW, int E, int STAGES = kBulkStages, int SB = kBulkStageBytes>
+static bool bulk_ref(ExactRef* r) {
+  *r = ExactRef{rd_exact_bulk_kernel<T, STAGES, SB, CW, E>, 32 * (CW + 1), STAGES, SB, RD_VARIANT_BULK,
+                BulkSmem<STAGES, SB, CW>::kBytes};
+  return true;
+}
+
+// Tuning only: RD_TUNE_EXACT_BULK="CW,E" (consumer warps, expansions)
 template <typename T>
 static bool pick_bulk(ExactRef* r) {
-  constexpr int CW = kExactBulkConsumerWarps;
-  *r = ExactRef{rd_exact_bulk_kernel<T, kBulkStages, kBulkStageBytes, CW, kExactExpansions>, 32 * (CW + 1),
-                kBulkStages, kBulkStageBytes, RD_VARIANT_BULK, BulkSmem<kBulkStages, kBulkStageBytes, CW>::kBytes};
-  return true;
+  static int tcw = 0, te = 0;
+  static bool once = [] {
+    const char* v = std::getenv("RD_TUNE_EXACT_BULK");
+    if (v && std::sscanf(v, "%d,%d", &tcw, &te) != 2) tcw = te = 0;
+    return true;
+  }();
+  (void)once;
+  const int cw = tcw ? tcw : kExactBulkConsumerWarps, e = te ? te : kExactBulkExpansions;
+  if (cw == 16 && e == 2) return bulk_ref<T, 16, 2>(r);
+  if (cw == 16 && e == 1) return bulk_ref<T, 16, 1>(r);
+  if (cw == 24 && e == 1) return bulk_ref<T, 24, 1, 5, 24576>(r);
+  if (cw == 24 && e == 2) return bulk_ref<T, 24, 2, 5, 24576>(r);
+  if (cw == 8 && e == 2) return bulk_ref<T, 8, 2>(r);
+  return false;
 }
 
 bool lookup_exact(int dtype, int variant, ExactRef* r) {

@@ -37,9 +37,11 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
                         rd_launch_info* info, const FusedArgs* fused = nullptr);
 
 // RD_SUM_EXACT on floats (rd_exact.cuh): mode 0 -> one element at `out`,
-// mode 1 -> one rd_exact_record at `xrec`; and the exact-record combine.
+// mode 1 -> one rd_exact_record at `xrec`, mode 2 -> the fused exchange of
+// `fused` (exact records in LL form); and the exact-record combine.
 rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, rd_exact_record* xrec,
-                       cudaStream_t stream, const rd_config* cfg, rd_launch_info* info);
+                       cudaStream_t stream, const rd_config* cfg, rd_launch_info* info,
+                       const FusedArgs* fused = nullptr);
 rd_status launch_exact_combine(const rd_exact_record* recs, int count, int dtype, void* out,
                                rd_exact_record* rec_out, int* d_status, cudaStream_t stream);
 

@@ -37,10 +37,14 @@ constexpr int kMaxRanks = 32;
 // 4 bytes of the 32-byte record and the 32-bit epoch, and is written with one
 // single-copy-atomic 8-byte store. A reader polls the 8 words until all carry
 // the expected epoch -- no fences, no release/acquire round trips.
+// Exact-sum records (rd_exact.cuh) travel the same way: 4 + 2 * 68 payload
+// words {tag, n lo, n hi, flags, word[0] lo, word[0] hi, ...} per sender.
+constexpr int kExactLLWords = 4 + 2 * 68;
 struct Mailbox {
   unsigned long long ll[2][kMaxRanks][8];  // [epoch parity][sender][word]
   unsigned long long epoch;                // calls completed by this rank (device-side:
                                            // the exchange is CUDA-graph capturable)
+  unsigned long long xll[2][kMaxRanks][kExactLLWords];   // exact records, same protocol
 };
 
 struct KArgs {

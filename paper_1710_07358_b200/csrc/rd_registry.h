@@ -43,6 +43,7 @@ constexpr int kExactUnroll = 6;       // 32-byte loads in flight per thread per 
 constexpr int kExactExpansions = 2;   // independent (a0, a1) expansions per thread
 constexpr int kExactMinBlocks = 2;    // __launch_bounds__ min CTAs/SM (register cap: <= 128)
 constexpr int kExactBulkConsumerWarps = 16;   // bulk variant: the fold is FP64-latency bound
+constexpr int kExactBulkExpansions = 1;       // bulk variant (tools/gpu/tune_exact_bulk.sh)
 bool lookup_exact(int dtype, int variant, ExactRef* r);
 ExactCombineFn lookup_exact_combine(int dtype);
 

@@ -97,7 +97,7 @@ def test_validation_before_any_device_work():
     assert L.reduce(p, 5, 0, 11, out, None) == 1                   # unknown op
     assert L.reduce_partial(p, 5, 3, 10, out, None) == 2           # exact float partial needs a wide record
     assert L.rd_combine_records(p, 1, 4, 10, out, None, None, None) == 2
-    assert L.reduce_fused(p, 4, 3, 10, out, None, None) == 1        # comm NULL comes first
+    assert L.reduce_fused(p, 4, 3, 10, out, None, None) == 1        # comm NULL
     assert L.reduce_exact_partial(p, 5, 0, out, None) == 2         # integer dtype: use reduce_partial
     assert L.reduce_exact_partial(None, 5, 3, out, None) == 1
     assert L.reduce_exact_partial(p + 2, 5, 3, out, None) == 3

@@ -540,12 +540,13 @@ def test_fused_exchange_local_ranks(rd, W):
     """reduce_fused with W virtual ranks on one GPU (mailboxes connected by
     pointer, kernels on W concurrent streams): every rank returns the identical
     result, equal to the oracle on the whole array, over several epochs (the
-    epoch-parity double buffering) and for plain, compensated and arg ops."""
+    epoch-parity double buffering) and for plain, compensated, exact and arg ops."""
     comms = rd.FusedComm.local(W, torch.cuda.current_device())
     streams = [torch.cuda.Stream() for _ in range(W)]
     try:
         cases = [("float32", "sum", (1 << 20) + 7), ("float64", "argmax", 100003), ("int32", "xor", 5533214),
-                 ("float64", "prod", (1 << 16) + 1), ("float32", "sum_compensated", 1 << 25), ("int64", "min", 7)]
+                 ("float64", "prod", (1 << 16) + 1), ("float32", "sum_compensated", 1 << 25), ("int64", "min", 7),
+                 ("float32", "sum_exact", (1 << 20) + 7), ("float64", "sum_exact", (1 << 25) + 3)]
         for rep in range(3):
             for dtype, op, n in cases:
                 x = inputs.generate(n, dtype, inputs.default_workload(dtype, op), seed=rep + 1)

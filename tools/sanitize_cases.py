@@ -42,10 +42,13 @@ def val(t):
 
 
 def main():
+    only = sys.argv[sys.argv.index("--only-op") + 1] if "--only-op" in sys.argv else None
     count = 0
     for dtype in ("int32", "uint32", "int64", "float32", "float64"):
         ops = FLT_OPS if dtype.startswith("float") else INT_OPS
         for op in ops:
+            if only and op != only:
+                continue
             wl = inputs.default_workload(dtype, op)
             for n, off in ((0, 0), (5, 1), (1000, 3), (70001, 2)):
                 x = inputs.generate(n, dtype, wl, seed=3)
@@ -54,6 +57,10 @@ def main():
                     out, _ = rd.reduce_ex(xd, op, variant=variant, grid=grid)
                     _parity.check(val(out), x, op)
                     count += 1
+    if only:
+        torch.cuda.synchronize()
+        print(f"sanitize cases ok: {count} launches checked ({only})")
+        return
     x = inputs.generate(100003, "float32", "u01", seed=1)
     xd = dev(x, 1)
     for f in (1, 8, 16):
