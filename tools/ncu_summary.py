@@ -19,6 +19,12 @@ KEYS = [
     "launch__occupancy_limit_registers", "launch__waves_per_multiprocessor",
     "sm__cycles_elapsed.avg.per_second", "dram__cycles_elapsed.avg.per_second",
     "lts__t_bytes.sum", "smsp__inst_executed.sum",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
 ]
 
 
