@@ -96,6 +96,7 @@ static void dd_add(double* hi, double* lo, double x) {
   if (!isfinite(*hi) || !isfinite(x)) { *hi = *hi + x; *lo = 0.0; return; }
   double s, e;
   two_sum(*hi, x, &s, &e);
+  if (!isfinite(s)) { *hi = s; *lo = 0.0; return; }   /* overflow: +-inf (TwoSum's error is NaN) */
   e += *lo;
   fast_two_sum(s, e, hi, lo);
 }

@@ -27,7 +27,9 @@ def _free_port():
 
 CASES = [("int32", "sum", "uniform_bits"), ("uint32", "and", "sparse_clear"), ("int64", "prod", "odd"),
          ("float32", "sum", "u01"), ("float64", "sum", "normalish"), ("float32", "max", "planted"),
-         ("float64", "prod", "near_one"), ("int32", "xor", "uniform_bits")]
+         ("float64", "prod", "near_one"), ("int32", "xor", "uniform_bits"),
+         # exact sums (reading R17): the rank-order merge of exact partials is bit-exact
+         ("float32", "sum_exact", "wide"), ("float64", "sum_exact", "wide_full")]
 
 
 def _worker(rank, world, port, outdir):

@@ -442,3 +442,14 @@ def test_arg_ops_block_merge(dtype):
             b = oracle.Fold(dtype, op).fold(x[cut:])
             got = a.merge(b).result()
             assert got.index == want.index and got.value == want.value
+
+
+def test_overflowing_double_double_sum_is_inf_not_nan():
+    """A finite fp64 sum whose running value overflows gives +inf (IEEE 754 overflow of a sum of
+    positive terms), in the value and in sum|x|; TwoSum's error term of an overflowed sum is NaN and
+    must not leak into the double-double accumulators."""
+    big = np.finfo(np.float64).max
+    r = oracle.reduce(np.array([big, big, 1.0], np.float64), "sum")
+    assert r.value == np.inf and r.sum_abs == np.inf
+    r = oracle.reduce(np.array([-big, -big], np.float64), "sum")
+    assert r.value == -np.inf and r.sum_abs == np.inf
