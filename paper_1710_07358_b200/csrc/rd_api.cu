@@ -321,6 +321,17 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     uint64_t need = (units + per_cta - 1) / per_cta;
     if (need < 1) need = 1;
     if (g > need) g = need;
+    // Mid sizes (the vector kernel runs below kBulkMinBytes): per-CTA costs
+    // (partial, ticket, the last CTA's fold) outweigh more resident CTAs --
+    // from 12 MiB, 1 CTA/SM up to 48 MiB and 2 above (tools/sweep.py midops,
+    // graph-captured, 7 (dtype, op): 7-16% faster at 16-64 MB; below 12 MiB
+    // the cap cost up to 12%, so it does not apply there).
+    static const uint64_t kMidCap = env_u64("RD_TUNE_VEC_CTAS_PER_SM", 0);
+    if (k.variant == RD_VARIANT_VECTOR && kMidCap != 1000 && (uint64_t)n * s >= (12ull << 20)) {
+      const uint64_t per_sm = kMidCap ? kMidCap : ((uint64_t)n * s >= (48ull << 20) ? 2 : 1);
+      const uint64_t cap = (uint64_t)di.sms * per_sm;
+      if (g > cap) g = cap;
+    }
   }
   if (cfg && cfg->grid > 0) g = (uint64_t)cfg->grid;
   if (g > (uint64_t)kMaxGrid) g = kMaxGrid;

@@ -424,11 +424,57 @@ __device__ __noinline__ void exact_fused_exchange(long long* words, unsigned fla
   }
 }
 
+// The end-of-thread deposit, warp-cooperative and without atomics: every
+// lane of the (converged) warp passes one double (0 = nothing); each stages
+// its three signed digits and word index, and lane j then adds, for word
+// kmin + j of the warp's window, the digits of all 32 lanes that land there.
+// (Per-lane shared 64-bit atomics are CAS loops on sm_100a, ATOMS.CAST.SPIN.64,
+// and all lanes hit the same words: that cost ~10 us per launch.) Safe
+// without atomics: only this warp writes its superaccumulator, and the
+// warp's slow-path atomics are complete (__syncwarp).
+struct XStage { long long k, s0, s1, s2; };
+template <typename T>
+__device__ __forceinline__ void sacc_flush_warp(long long* w, XStage* stage, double d) {
+  using TR = ExactTraits<T>;
+  const int ln = threadIdx.x & 31;
+  long long k = -1000, s0 = 0, s1 = 0, s2 = 0;
+  if (d != 0.0) {
+    const uint64_t b = (uint64_t)__double_as_longlong(d);
+    int e = (int)((b >> 52) & 0x7ff);
+    uint64_t m = b & ((1ull << 52) - 1);
+    if (e) m |= 1ull << 52;
+    else e = 1;
+    int p = e - 1075 - TR::kLsb;
+    if (p < 0) { m >>= -p; p = 0; }
+    const int r = p & 31;
+    const uint64_t lo = m << r;
+    s0 = (long long)(lo & 0xffffffffull);
+    s1 = (long long)(lo >> 32);
+    s2 = r ? (long long)(m >> (64 - r)) : 0;
+    if ((int64_t)b < 0) { s0 = -s0; s1 = -s1; s2 = -s2; }
+    k = p >> 5;
+  }
+  const int kmin = __reduce_min_sync(0xffffffffu, (int)(k < 0 ? 0x7fffffff : k));
+  const int kmax = __reduce_max_sync(0xffffffffu, (int)k);
+  if (kmax < 0) return;                              // warp-uniform: nothing to add
+  stage[ln] = XStage{k, s0, s1, s2};
+  __syncwarp();
+  for (int word = kmin + ln; word <= kmax + 2; word += 32) {
+    long long acc = 0;
+    for (int l = 0; l < 32; ++l) {
+      const XStage q = stage[l];                     // broadcast read
+      acc += (q.k == word ? q.s0 : 0) + (q.k + 1 == word ? q.s1 : 0) + (q.k + 2 == word ? q.s2 : 0);
+    }
+    w[word] += acc;                                  // |acc| < 2^37
+  }
+  __syncwarp();
+}
+
 // a3-a7, shared by both exact kernels: expansions -> warp superaccumulators
 // -> the CTA's slot -> (last CTA) the sum of the G slots, rounded once.
 template <typename T, int B, int E>
 __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
-                                             long long* tot, unsigned& s_flags, unsigned& s_last,
+                                             long long* tot, XStage (*stage)[32], unsigned& s_flags, unsigned& s_last,
                                              const XArgs& args) {
   constexpr int NW = ExactTraits<T>::kWords;
   constexpr int NWARP = B / 32;
@@ -438,12 +484,13 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
   // through some a0 (or the slow path, which flags itself), and an a0 that
   // has seen a term other than -0.0 is never -0.0 again (x + -x = +0), so a0
   // alone decides reading R2's "every term is -0.0".
+  __syncwarp();
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     if ((uint64_t)__double_as_longlong(ex[j].a0) != kNegZeroBits) flags |= kXNotNegZero;
-    if (ex[j].a0 != 0.0) sacc_add<T>(w, ex[j].a0);
-    if (ex[j].a1 != 0.0) sacc_add<T>(w, ex[j].a1);
-    if (ex[j].a2 != 0.0) sacc_add<T>(w, ex[j].a2);
+    sacc_flush_warp<T>(w, stage[warp], ex[j].a0);
+    sacc_flush_warp<T>(w, stage[warp], ex[j].a1);
+    sacc_flush_warp<T>(w, stage[warp], ex[j].a2);
   }
   flags = __reduce_or_sync(0xffffffffu, flags);
   if (ln == 0 && flags) atomicOr(&s_flags, flags);
@@ -527,6 +574,7 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
   constexpr int NWARP = B / 32;
   __shared__ long long sacc[NWARP][NW];
   __shared__ long long tot[B];
+  __shared__ XStage stage[B / 32][32];
   __shared__ unsigned s_flags, s_last;
 
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -576,7 +624,7 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
   // a2: head and tail stragglers
   if (tid < args.head) ex_add<T>(ex[0], widen(ldg_scalar<T>(args.x + tid * sizeof(T))), w, flags);
   if (tid < args.tail) ex_add<T>(ex[1], widen(ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T))), w, flags);
-  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
+  exact_finish<T, B, E>(ex, flags, sacc, tot, stage, s_flags, s_last, args);
 }
 
 // The bulk-copy form (like rd_bulk_kernel): one producer lane streams
@@ -601,6 +649,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const X
   uint32_t* st_bytes = reinterpret_cast<uint32_t*>(empty + STAGES);   // 0 = no more chunks
   __shared__ long long sacc[B / 32][NW];
   __shared__ long long tot[B];
+  __shared__ XStage stage[B / 32][32];
   __shared__ unsigned s_flags, s_last;
 
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -700,7 +749,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const X
     }
   }
   pdl_trigger();
-  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
+  exact_finish<T, B, E>(ex, flags, sacc, tot, stage, s_flags, s_last, args);
 }
 
 // Fold `count` exact records (any order gives the same integer): one CTA.

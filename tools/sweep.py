@@ -224,6 +224,75 @@ def do_sizes(args):
     return rows
 
 
+def graph_us(fn, reps=100):
+    """per-launch time of `reps` launches captured in one CUDA graph (no host overhead)"""
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=gs):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    ts = []
+    for _ in range(7):                       # median of 7 replays (clock / power noise)
+        c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c.record(s)
+        g.replay()
+        d.record(s)
+        d.synchronize()
+        ts.append(c.elapsed_time(d) * 1e3 / reps)
+    return statistics.median(ts)
+
+
+def do_midgrids(args):
+    """Mid sizes (2^16..2^27): grid and variant vs cold single-launch and graph-captured time."""
+    rows = []
+    for log2n in range(16, 28):
+        n = 1 << log2n
+        x = make(n, "float32", "u01")
+        o = torch.empty((), dtype=x.dtype, device="cuda")
+        _, info = rd.reduce_ex(x, "sum", out=o)
+        for variant in ("vector", "bulk"):
+            for g in (0, 37, 74, 148, 296, 444, 592, 888):
+                try:
+                    _, inf2 = rd.reduce_ex(x, "sum", variant=variant, grid=g, out=o)
+                except rd.ReduceError:
+                    continue
+                fn = lambda: rd.reduce_ex(x, "sum", variant=variant, grid=g, out=o)
+                cold = time_launch(fn, n * 4, reps=20)
+                r = {"n": n, "log2n": log2n, "variant": variant, "grid": inf2["grid"], "auto_grid": info["grid"],
+                     "auto_variant": info["variant"], "cold_us": cold["t_med_us"], "graph_us": graph_us(fn)}
+                rows.append(r)
+                print(json.dumps(r), flush=True)
+        del x
+    return rows
+
+
+def do_midops(args):
+    """Mid sizes, the AUTO plan for several (dtype, op): graph-captured us per launch
+    (A/B the planner with RD_TUNE_VEC_CTAS_PER_SM: 1000 = uncapped)."""
+    rows = []
+    for dtype, op in (("float32", "sum"), ("int32", "sum"), ("float64", "sum"), ("float32", "argmin"),
+                      ("float64", "prod"), ("float32", "sum_exact"), ("int64", "xor")):
+        for log2n in range(18, 26):
+            n = 1 << log2n
+            x = make(n, dtype, inputs.default_workload(dtype, op) if op != "sum_exact" else "u01")
+            o = torch.empty(2, dtype=torch.int64, device="cuda") if op in rd.ARG_OPS else \
+                torch.empty((), dtype=x.dtype, device="cuda")
+            _, info = rd.reduce_ex(x, op, out=o)
+            r = {"dtype": dtype, "op": op, "log2n": log2n, "variant": info["variant"], "grid": info["grid"],
+                 "graph_us": graph_us(lambda: rd.reduce(x, op, out=o)),
+                 "cap": os.environ.get("RD_TUNE_VEC_CTAS_PER_SM", "default")}
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+            del x
+    return rows
+
+
 def do_grids(args):
     """Grid multiplier (waves of resident CTAs) for the default kernels at n = 2^28."""
     rows = []
@@ -357,14 +426,15 @@ def do_overhead(args):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi", "overhead",
-                                    "exact"])
+                                    "exact", "midgrids", "midops"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
     args = p.parse_args()
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
            "grids": do_grids, "crossover": do_crossover, "multi": do_multi,
-           "overhead": do_overhead, "exact": do_exact}[args.what](args)
+           "overhead": do_overhead, "exact": do_exact,
+           "midgrids": do_midgrids, "midops": do_midops}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
         json.dump({"meta": meta, "result": res}, f, indent=1)
