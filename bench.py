@@ -344,6 +344,20 @@ def run_b200(args):
             b.record(stream)
             torch.cuda.synchronize(dev)
             tctx = round(gbps(n * s * 20, a.elapsed_time(b) / 1e3), 2)
+        # ... and this library's reproducible variants of the same sum on the same
+        # tensor (not the bench value): compensated and exact-rounded-once
+        variants = {}
+        if op == "sum" and not args.profile and x.is_floating_point():
+            for vop in ("sum_compensated", "sum_exact"):
+                for _ in range(3):
+                    rd.reduce(x, vop, out=out)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(20):
+                    rd.reduce(x, vop, out=out)
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                variants[vop + "_gbs"] = round(gbps(n * s * 20, a.elapsed_time(b) / 1e3), 2)
 
         # ---------------- cpu_baseline: the oracle on the host, rank 0, N = 1 only
         cpu = None
@@ -399,7 +413,7 @@ def run_b200(args):
             "e2e": e2e,
             "gpu_launches": K * (1 if (comm is None or exchange == "fused") else 2),
             "clocks": clocks,
-            "context": {"torch_sum_gbs": tctx, "result": res},
+            "context": {"torch_sum_gbs": tctx, "result": res, **variants},
         }
         emit(line)
     if use_comm:
