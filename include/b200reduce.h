@@ -42,10 +42,12 @@
  *  - float x: fp32 accumulates in fp64, fp64 in double-double, then one
  *    rounding; |result - exact| <= 4 * eps(dtype) * |exact| when no partial
  *    product over/underflows.
+ *  - float exact sum (RD_SUM_EXACT): the real sum rounded once -- the same
+ *    bits for every grid, variant, base alignment, shard split and GPU count.
  *  - Determinism: identical (x, n, base alignment, dtype, op, device) give
  *    identical bits (no float atomics; every combine is in a fixed order).
  *
- *  empty results:   +   x    min          max          and   or  xor
+ *  empty results:   +   x    min          max          and   or  xor   (+ compensated / exact: as +)
  *      int32        0   1    INT32_MAX    INT32_MIN    -1    0   0
  *      uint32       0   1    UINT32_MAX   0            ~0u   0   0
  *      int64        0   1    INT64_MAX    INT64_MIN    -1    0   0
@@ -292,6 +294,9 @@ const char* rd_last_error(void);
  *   unroll    loads in flight per thread per iteration (U; the paper's F);
  *             ring stages (BULK variant)
  *   grid      CTAs (clamped to [1, 4096])
+ * RD_SUM_EXACT on floats has one compiled kernel per variant (vector: 32-byte
+ * loads, U = 6; bulk: the default ring with 16 consumer warps): only variant
+ * and grid may be chosen.
  * The chosen configuration is written to *info (may be NULL).
  * Configurations without a compiled kernel return RD_ERR_UNSUPPORTED. */
 enum { RD_VARIANT_AUTO = 0, RD_VARIANT_VECTOR = 1, RD_VARIANT_PAPER = 2, RD_VARIANT_BULK = 3 };
