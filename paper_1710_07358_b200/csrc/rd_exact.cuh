@@ -5,22 +5,25 @@
 // the exact sum is the one result no order, grid, variant, base alignment or
 // GPU count can change -- so it is bitwise reproducible by construction.
 //
-// Design (one single-pass launch, like rd_vector_kernel):
-//  a1  each thread streams 32-byte vectors grid-stride and adds every element
-//      (fp32 widened to fp64, exactly) into one of E = 4 two-term expansions
-//      (a0, a1) with an error-free TwoSum: a0 + x = s + e exactly. When e == 0
-//      (every term for data whose exponents span < ~29 bits below the running
-//      sum -- the u01 / normal workloads) that is the whole cost: 6 DADD and
-//      one compare per element. A nonzero e goes into a1 by a second TwoSum,
-//      and only a nonzero second error -- or an fp64 overflow, or inf/NaN --
-//      takes the rare slow path into the warp's superaccumulator.
+// Design (one single-pass launch; a vector-load and a bulk-copy form):
+//  a1  each thread streams vectors (32-byte loads, or LDS.128 from the bulk
+//      ring) and adds every element (fp32 widened to fp64, exactly) into one
+//      of E three-term expansions (a0, a1, a2), a0 + a1 + a2 exact. Per
+//      vector it SPECULATES branch-free -- fp32 data: every add into a0 is
+//      exact, tested by compares only (fl(s - a0) == x && fl(s - x) == a0;
+//      3 DADD + 2 compares per element); fp64 data: a0's TwoSum error goes into
+//      a1 exactly -- with ONE branch per vector. A failed vector is replayed
+//      element by element out of line (replay_vec: a0 -> a1 -> a2 TwoSums;
+//      only a nonzero third error, an fp64 overflow or inf/NaN reaches the
+//      superaccumulator). Loops end with __syncwarp so replays reconverge.
 //  superaccumulator: a fixed-point integer whose unit is the dtype's smallest
 //      subnormal (2^-149 / 2^-1074), held as kWords carry-save int64 words of
 //      32-bit digits in shared memory (one per warp). A finite double is
 //      deposited exactly as three signed digits (shared 64-bit atomics); a word
 //      nearing 2^60 moves its high part to the next word (value-preserving).
-//  a3-a5  at the end every thread deposits its expansions; each warp carries
-//      its words to digits in [0, 2^32); the CTA adds the W warps' digits.
+//  a3-a5  at the end the warp deposits its lanes' expansions cooperatively
+//      (no atomics), carries its words to digits in [0, 2^32), and the CTA
+//      adds its warps' digits.
 //  a6  the CTA's words go to workspace slot blockIdx; the last CTA (atomic
 //      ticket) adds the G slots word by word (integers: any order is exact),
 //      carries, and
@@ -29,7 +32,9 @@
 //      the float is assembled as (shift << (p-1)) + q, which carries a rounded-
 //      up mantissa into the exponent and reaches inf exactly at the IEEE
 //      overflow threshold. Specials: flags for NaN, +inf, -inf and "some term
-//      is not -0.0" (reading R2's sign of a zero sum).
+//      is not -0.0" (reading R2's sign of a zero sum). Or (mode 1) the carried
+//      words leave as an rd_exact_record, or (mode 2) go through the fused
+//      multi-GPU mailboxes (exact_fused_exchange).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
