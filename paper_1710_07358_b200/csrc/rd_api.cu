@@ -151,20 +151,25 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
   return x ? (uint64_t)x : dflt;
 }
 
-// Bulk chunk schedule, fixed by the body size and the stage size only
-// (determinism): a head region in chunks of C0 (about 16 per SM, at most
-// 5000), then a tail region of 148*16 chunks of C1 = one stage, so the
+// Bulk chunk schedule, fixed by the body size, the stage size and the op
+// class only (determinism): a head region in chunks of C0 (about 16 per SM,
+// at most 5000), then a tail region of 148*P chunks of C1 = Q stages, so the
 // dynamic schedule ends with short chunks and the per-SM tail imbalance is
-// < one C1 chunk. (16/16/1 measured best of a sweep, tools/tune_bulk.sh:
-// +0.9% over 12/4/2.)
+// < one C1 chunk. Plain ops: P = 16, Q = 1 (measured best of a sweep,
+// tools/tune_bulk.sh: +0.9% over 12/4/2). Indexed ops (argmin / argmax) pay
+// more per chunk end (the (key, index) tree), so they take fewer, longer tail
+// chunks: P = 4, Q = 4 (tools/ab_lib.py, one box: float32 argmin 6.45 ->
+// 6.82 TB/s, int32 argmax 6.92 -> 7.18, float64 argmin 7.03 -> 7.20).
 struct BulkPlan {
   uint64_t c0, c1, head_region;
   uint32_t nhead, nchunks;
 };
-bool plan_bulk(uint64_t body_bytes, uint64_t stage_bytes, BulkPlan* p) {
+bool plan_bulk(uint64_t body_bytes, uint64_t stage_bytes, BulkPlan* p, bool indexed = false) {
   static const uint64_t kHeadPerSm = env_u64("RD_TUNE_HEAD_PER_SM", 16);
-  static const uint64_t kTailPerSm = env_u64("RD_TUNE_TAIL_PER_SM", 16);
-  static const uint64_t kTailStages = env_u64("RD_TUNE_TAIL_STAGES", 1);
+  static const uint64_t kTailPerSmEnv = env_u64("RD_TUNE_TAIL_PER_SM", 0);
+  static const uint64_t kTailStagesEnv = env_u64("RD_TUNE_TAIL_STAGES", 0);
+  const uint64_t kTailPerSm = kTailPerSmEnv ? kTailPerSmEnv : (indexed ? 4 : 16);
+  const uint64_t kTailStages = kTailStagesEnv ? kTailStagesEnv : (indexed ? 4 : 1);
   const uint64_t T = body_bytes;
   const uint64_t S = stage_bytes;
   const uint64_t C1 = kTailStages * S;
@@ -301,7 +306,7 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   }
   if (k.variant == RD_VARIANT_BULK) {
     BulkPlan bp;
-    if (!plan_bulk(a.nvec * 16, (uint64_t)k.vec_bytes, &bp)) {
+    if (!plan_bulk(a.nvec * 16, (uint64_t)k.vec_bytes, &bp, is_arg_op(op))) {
       set_error("chunk schedule exceeds the workspace");
       return RD_ERR_INVALID_ARG;
     }

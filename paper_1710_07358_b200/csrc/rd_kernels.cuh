@@ -212,7 +212,7 @@ __device__ __forceinline__ void fold_records_warp(int count, uint32_t tag, Load 
 // no host call, no second kernel and no memory fence. A bounded wait reports
 // RD_ERR_TIMEOUT.
 template <class OpT>
-__device__ __noinline__ void fused_exchange(typename OpT::Acc a, const KArgs& args) {
+__device__ __forceinline__ void fused_exchange(typename OpT::Acc a, const KArgs& args) {
   const int ln = threadIdx.x & 31;
   Slot s = OpT::pack(a);                               // valid in lane 0
   s.a = __shfl_sync(0xffffffffu, s.a, 0);

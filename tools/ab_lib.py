@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""A/B of library builds on the same box: back-to-back GB/s of `reduce` for a
+few (dtype, op) at n = 2^28, through ctypes on each .so given (measurement
+only).   python tools/ab_lib.py build/ab/lib_a.so build/ab/lib_b.so ..."""
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+
+DT = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
+OPS = {"sum": 0, "max": 3, "argmin": 7, "argmax": 8}
+PAIRS = [("float32", "argmin"), ("float32", "argmax"), ("int32", "argmax"), ("float64", "argmin"),
+         ("float32", "sum"), ("int32", "sum")]
+
+
+def run(path, x_by_dtype):
+    L = ctypes.CDLL(path)
+    L.reduce.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    L.reduce.restype = ctypes.c_int
+    out = torch.empty(2, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream()
+    res = {}
+    for dtype, op in PAIRS:
+        x = x_by_dtype[dtype]
+        f = lambda: L.reduce(x.data_ptr(), x.numel(), DT[dtype], OPS[op], out.data_ptr(), st.cuda_stream)
+        for _ in range(5):
+            assert f() == 0
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            for _ in range(20):
+                f()
+            b.record(st)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) / 20 * 1e-3)
+        ts.sort()
+        res[f"{dtype}-{op}"] = round(x.numel() * x.element_size() / ts[2] / 1e9, 1)
+    return res
+
+
+if __name__ == "__main__":
+    n = 1 << 28
+    xs = {}
+    for dtype in ("float32", "int32", "float64"):
+        xs[dtype] = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
+        inputs.fill_device(xs[dtype], "u01" if dtype.startswith("float") else "int_small", seed=1)
+    for rnd in range(2):                      # interleaved twice: clock drift shows up
+        for p in sys.argv[1:]:
+            print(json.dumps({"lib": os.path.basename(p), "round": rnd, **run(p, xs)}), flush=True)
