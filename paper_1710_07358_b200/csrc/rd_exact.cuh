@@ -429,48 +429,67 @@ __device__ __noinline__ void exact_fused_exchange(long long* words, unsigned fla
   }
 }
 
-// The end-of-thread deposit, warp-cooperative and without atomics: every
-// lane of the (converged) warp passes one double (0 = nothing); each stages
-// its three signed digits and word index, and lane j then adds, for word
-// kmin + j of the warp's window, the digits of all 32 lanes that land there.
-// (Per-lane shared 64-bit atomics are CAS loops on sm_100a, ATOMS.CAST.SPIN.64,
-// and all lanes hit the same words: that cost ~10 us per launch.) Safe
-// without atomics: only this warp writes its superaccumulator, and the
-// warp's slow-path atomics are complete (__syncwarp).
-struct XStage { long long k, s0, s1, s2; };
-template <typename T>
-__device__ __forceinline__ void sacc_flush_warp(long long* w, XStage* stage, double d) {
+// The end-of-thread deposit, warp-cooperative, in registers and without
+// atomics: every lane of the (converged) warp passes its NV doubles (0 =
+// nothing). The warp walks the superaccumulator words its lanes' digits land
+// in (the next occupied word comes from one redux.min); per word each lane
+// sums its own digits there (|c| < 2^35), the warp adds the 32 lane sums with
+// three 13-bit-chunk redux.sync adds (offset to be nonnegative: no chunk sum
+// overflows), and lane 0 adds the total to the word. (Per-lane shared 64-bit
+// atomics are CAS loops on sm_100a, ATOMS.CAST.SPIN.64, and a smem-staged
+// transposed sum costs ~2000 instructions per warp: both dominated small n.)
+// Only this warp writes its superaccumulator, and its slow-path atomics are
+// complete (__syncwarp).
+template <typename T, int NV>
+__device__ __forceinline__ void sacc_flush_warp(long long* w, const double (&d)[NV]) {
   using TR = ExactTraits<T>;
-  const int ln = threadIdx.x & 31;
-  long long k = -1000, s0 = 0, s1 = 0, s2 = 0;
-  if (d != 0.0) {
-    const uint64_t b = (uint64_t)__double_as_longlong(d);
-    int e = (int)((b >> 52) & 0x7ff);
-    uint64_t m = b & ((1ull << 52) - 1);
-    if (e) m |= 1ull << 52;
-    else e = 1;
-    int p = e - 1075 - TR::kLsb;
-    if (p < 0) { m >>= -p; p = 0; }
-    const int r = p & 31;
-    const uint64_t lo = m << r;
-    s0 = (long long)(lo & 0xffffffffull);
-    s1 = (long long)(lo >> 32);
-    s2 = r ? (long long)(m >> (64 - r)) : 0;
-    if ((int64_t)b < 0) { s0 = -s0; s1 = -s1; s2 = -s2; }
-    k = p >> 5;
-  }
-  const int kmin = __reduce_min_sync(0xffffffffu, (int)(k < 0 ? 0x7fffffff : k));
-  const int kmax = __reduce_max_sync(0xffffffffu, (int)k);
-  if (kmax < 0) return;                              // warp-uniform: nothing to add
-  stage[ln] = XStage{k, s0, s1, s2};
-  __syncwarp();
-  for (int word = kmin + ln; word <= kmax + 2; word += 32) {
-    long long acc = 0;
-    for (int l = 0; l < 32; ++l) {
-      const XStage q = stage[l];                     // broadcast read
-      acc += (q.k == word ? q.s0 : 0) + (q.k + 1 == word ? q.s1 : 0) + (q.k + 2 == word ? q.s2 : 0);
+  constexpr int kNone = 0x7fffffff;
+  int k[NV];
+  long long s0[NV], s1[NV], s2[NV];
+  int first = kNone;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    k[v] = kNone;
+    s0[v] = s1[v] = s2[v] = 0;
+    if (d[v] != 0.0) {
+      const uint64_t b = (uint64_t)__double_as_longlong(d[v]);
+      int e = (int)((b >> 52) & 0x7ff);
+      uint64_t m = b & ((1ull << 52) - 1);
+      if (e) m |= 1ull << 52;
+      else e = 1;
+      int p = e - 1075 - TR::kLsb;
+      if (p < 0) { m >>= -p; p = 0; }
+      const int r = p & 31;
+      const uint64_t lo = m << r;
+      s0[v] = (long long)(lo & 0xffffffffull);
+      s1[v] = (long long)(lo >> 32);
+      s2[v] = r ? (long long)(m >> (64 - r)) : 0;
+      if ((int64_t)b < 0) { s0[v] = -s0[v]; s1[v] = -s1[v]; s2[v] = -s2[v]; }
+      k[v] = p >> 5;
+      first = min(first, k[v]);
     }
-    w[word] += acc;                                  // |acc| < 2^37
+  }
+  int word = __reduce_min_sync(0xffffffffu, first);
+  while (word != kNone) {                            // warp-uniform
+    long long c = 0;
+    int next = kNone;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      c += (k[v] == word ? s0[v] : 0) + (k[v] + 1 == word ? s1[v] : 0) + (k[v] + 2 == word ? s2[v] : 0);
+      // this lane's next occupied word above `word` (k, k+1, k+2 of each value)
+      if (k[v] != kNone) {
+        const int d0 = k[v] - word;                  // in [-2, inf)
+        const int cand = d0 > 0 ? k[v] : (d0 > -2 ? k[v] + 2 - (d0 == 0 ? 1 : 0) : kNone);
+        next = min(next, cand);
+      }
+    }
+    const unsigned long long u = (unsigned long long)(c + (1ll << 38));   // in [0, 2^39)
+    const unsigned c0 = __reduce_add_sync(0xffffffffu, (unsigned)(u & 0x1fff));
+    const unsigned c1 = __reduce_add_sync(0xffffffffu, (unsigned)((u >> 13) & 0x1fff));
+    const unsigned c2 = __reduce_add_sync(0xffffffffu, (unsigned)(u >> 26));
+    if ((threadIdx.x & 31) == 0)
+      w[word] += (long long)c0 + ((long long)c1 << 13) + ((long long)c2 << 26) - (32ll << 38);
+    word = __reduce_min_sync(0xffffffffu, next);
   }
   __syncwarp();
 }
@@ -479,7 +498,7 @@ __device__ __forceinline__ void sacc_flush_warp(long long* w, XStage* stage, dou
 // -> the CTA's slot -> (last CTA) the sum of the G slots, rounded once.
 template <typename T, int B, int E>
 __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
-                                             long long* tot, XStage (*stage)[32], unsigned& s_flags, unsigned& s_last,
+                                             long long* tot, unsigned& s_flags, unsigned& s_last,
                                              const XArgs& args) {
   constexpr int NW = ExactTraits<T>::kWords;
   constexpr int NWARP = B / 32;
@@ -490,13 +509,15 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
   // has seen a term other than -0.0 is never -0.0 again (x + -x = +0), so a0
   // alone decides reading R2's "every term is -0.0".
   __syncwarp();
+  double dv[3 * E];
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     if ((uint64_t)__double_as_longlong(ex[j].a0) != kNegZeroBits) flags |= kXNotNegZero;
-    sacc_flush_warp<T>(w, stage[warp], ex[j].a0);
-    sacc_flush_warp<T>(w, stage[warp], ex[j].a1);
-    sacc_flush_warp<T>(w, stage[warp], ex[j].a2);
+    dv[3 * j] = ex[j].a0;
+    dv[3 * j + 1] = ex[j].a1;
+    dv[3 * j + 2] = ex[j].a2;
   }
+  sacc_flush_warp<T, 3 * E>(w, dv);
   flags = __reduce_or_sync(0xffffffffu, flags);
   if (ln == 0 && flags) atomicOr(&s_flags, flags);
   __syncwarp();
@@ -571,7 +592,7 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
 
 // --------------------------------------------------------------------- kernel
 template <typename T, int B, int U, int E, int MINB>
-__global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
+__global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const __grid_constant__ XArgs args) {
   using TR = ExactTraits<T>;
   constexpr int NW = TR::kWords;
   constexpr int VB = 32;
@@ -579,7 +600,6 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
   constexpr int NWARP = B / 32;
   __shared__ long long sacc[NWARP][NW];
   __shared__ long long tot[B];
-  __shared__ XStage stage[B / 32][32];
   __shared__ unsigned s_flags, s_last;
 
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -629,7 +649,7 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
   // a2: head and tail stragglers
   if (tid < args.head) ex_add<T>(ex[0], widen(ldg_scalar<T>(args.x + tid * sizeof(T))), w, flags);
   if (tid < args.tail) ex_add<T>(ex[1], widen(ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T))), w, flags);
-  exact_finish<T, B, E>(ex, flags, sacc, tot, stage, s_flags, s_last, args);
+  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
 }
 
 // The bulk-copy form (like rd_bulk_kernel): one producer lane streams
@@ -639,7 +659,7 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const XArgs args) {
 // ring (STAGES * STAGE_BYTES in flight per SM), not from registers -- the
 // vector kernel's 118 registers/thread cap it at 16 warps/SM.
 template <typename T, int STAGES, int STAGE_BYTES, int CW, int E>
-__global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const XArgs args) {
+__global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const __grid_constant__ XArgs args) {
   using TR = ExactTraits<T>;
   constexpr int NW = TR::kWords;
   constexpr int B = 32 * (CW + 1);
@@ -654,7 +674,6 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const X
   uint32_t* st_bytes = reinterpret_cast<uint32_t*>(empty + STAGES);   // 0 = no more chunks
   __shared__ long long sacc[B / 32][NW];
   __shared__ long long tot[B];
-  __shared__ XStage stage[B / 32][32];
   __shared__ unsigned s_flags, s_last;
 
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -754,7 +773,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const X
     }
   }
   pdl_trigger();
-  exact_finish<T, B, E>(ex, flags, sacc, tot, stage, s_flags, s_last, args);
+  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
 }
 
 // Fold `count` exact records (any order gives the same integer): one CTA.
