@@ -23,6 +23,21 @@
 
 namespace rd {
 
+// Releasing a ring stage: the consumers' generic-proxy READS of the stage are
+// ordered before the producer's next async-proxy WRITE (cp.async.bulk) by the
+// mbarrier alone -- arrive (release) on EMPTY, the producer's try_wait
+// (acquire), then the copy -- as in CUTLASS's consumer_release for TMA-load
+// pipelines (a proxy fence is needed for generic WRITES read by the async
+// proxy, e.g. before a TMA store). The fence.proxy.async that used to precede
+// the arrive cost 1.2-2.3% on the ALU-heavier ops and 5.5% on the exact sum
+// (an A/B of builds, profiles/ab/r01_ab_release_fence.jsonl); define
+// RD_RELEASE_PROXY_FENCE to restore it.
+#ifdef RD_RELEASE_PROXY_FENCE
+#define RD_RELEASE_FENCE() asm volatile("fence.proxy.async.shared::cta;" ::: "memory")
+#else
+#define RD_RELEASE_FENCE() ((void)0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -190,12 +205,12 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
           }
         }
       }
-      // release the stage: this warp's generic-proxy reads of the ring (and of
-      // the stage metadata) are ordered before the producer's next async-proxy
-      // (cp.async.bulk) write into it by the proxy fence + mbarrier release
+      // release the stage: this warp's reads of the ring (and of the stage
+      // metadata) are ordered before the producer's next cp.async.bulk write
+      // into it by the warp barrier + mbarrier release (RD_RELEASE_FENCE)
       __syncwarp();
       if (ln == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        RD_RELEASE_FENCE();
         mbar_arrive(&empty[stage]);
       }
       ++cstage;

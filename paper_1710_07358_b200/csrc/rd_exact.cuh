@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
       // reconverge (a replayed vector diverges), then release the stage
       __syncwarp();
       if (ln == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        RD_RELEASE_FENCE();
         mbar_arrive(&empty[stage]);
       }
       if (++stage == STAGES) { stage = 0; phase ^= 1; }

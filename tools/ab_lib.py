@@ -14,9 +14,11 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 
 DT = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
-OPS = {"sum": 0, "max": 3, "argmin": 7, "argmax": 8}
+OPS = {"sum": 0, "max": 3, "argmin": 7, "argmax": 8, "sum_exact": 10}
 PAIRS = [("float32", "argmin"), ("float32", "argmax"), ("int32", "argmax"), ("float64", "argmin"),
-         ("float32", "sum"), ("int32", "sum")]
+         ("float32", "sum"), ("int32", "sum"), ("float64", "max")]
+if os.environ.get("AB_EXACT"):
+    PAIRS.append(("float32", "sum_exact"))
 
 
 def run(path, x_by_dtype):
