@@ -359,6 +359,38 @@ def run_b200(args):
                 torch.cuda.synchronize(dev)
                 variants[vop + "_gbs"] = round(gbps(n * s * 20, a.elapsed_time(b) / 1e3), 2)
 
+        # ---------------- the same-run HBM read ceiling (SURVEY §8(d) peak 3): the read
+        # probe (tools/probe.cu: 256-bit loads xor-folded, no reduction semantics) over
+        # the same tensor, in its best configurations of profiles/r01_read_probe.json,
+        # back to back like the timed steps; the north star's ">= 90% of measured HBM
+        # read bandwidth" is value / this
+        probe = None
+        probe_lib = os.path.join(ROOT, "tools", "libprobe.so")
+        if not args.profile and os.path.exists(probe_lib):
+            import ctypes
+            pl = ctypes.CDLL(probe_lib)
+            pl.probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+            pl.probe_occupancy.argtypes = [ctypes.c_int, ctypes.c_int]
+            sink = torch.zeros(1024, dtype=torch.int32, device=dev)
+            best = 0.0
+            for thr, unr in ((256, 2), (1024, 2), (512, 1)):
+                blocks = 148 * max(1, pl.probe_occupancy(unr, thr)) * 4
+                fn = lambda: pl.probe_read(x.data_ptr(), n * s, unr, blocks, thr, sink.data_ptr(),
+                                           stream.cuda_stream, 0)
+                for _ in range(3):
+                    fn()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(20):
+                    fn()
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                best = max(best, gbps(n * s * 20, a.elapsed_time(b) / 1e3))
+            probe = {"value": round(best, 2), "unit": "GB/s", "frac": round(achieved / best, 4),
+                     "how": "tools/probe.cu read probe on the same tensor, best of 3 configs, 20 back-to-back "
+                            "launches each (CUDA events)"}
+
         # ---------------- cpu_baseline: the oracle on the host, rank 0, N = 1 only
         cpu = None
         if ws == 1 and not args.no_cpu and not args.profile:
@@ -408,7 +440,8 @@ def run_b200(args):
                          "traffic": load_traffic(f"{dt}-{op}-2^{args.log2n}"),
                          "kernel_ms": round(kern_ms, 5), "peak_source": peak_src,
                          "achieved_source": kern_src,
-                         "algorithmic_bytes_per_launch": n * s},
+                         "algorithmic_bytes_per_launch": n * s,
+                         "read_probe": probe},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": K * (1 if (comm is None or exchange == "fused") else 2),

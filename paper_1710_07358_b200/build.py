@@ -6,6 +6,8 @@
 - inputs/libinputs_host.so, inputs/libinputs_device.so   seeded generators
 - oracle/liboracle.so                       the CPU checker (test infrastructure;
                                             building it is not using it)
+- tools/libprobe.so                         the HBM read-bandwidth probe (measurement
+                                            tooling: bench.py's same-run read ceiling)
 """
 from __future__ import annotations
 
@@ -71,13 +73,24 @@ def build_library(force: bool = False) -> str:
     return LIB
 
 
+def build_probe(force: bool = False) -> str:
+    src = os.path.join(ROOT, "tools", "probe.cu")
+    out = os.path.join(ROOT, "tools", "libprobe.so")
+    if force or _stale(out, [src]):
+        subprocess.check_call(["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+                               src, "-o", out + ".tmp"])
+        os.replace(out + ".tmp", out)
+    return out
+
+
 def build_all(force: bool = False) -> None:
     sys.path.insert(0, ROOT)
     import inputs
     import oracle
-    with cf.ThreadPoolExecutor(max_workers=3) as ex:
+    with cf.ThreadPoolExecutor(max_workers=4) as ex:
         futs = [ex.submit(build_library, force), ex.submit(inputs.build_device, force),
-                ex.submit(inputs.build_host, force), ex.submit(oracle.build, force)]
+                ex.submit(inputs.build_host, force), ex.submit(oracle.build, force),
+                ex.submit(build_probe, force)]
         for f in futs:
             f.result()
 
