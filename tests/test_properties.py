@@ -78,3 +78,22 @@ def test_gpu_int_arbitrary(dtype, op, data):
     grid = data.draw(st.sampled_from([0, 1, 3, 200]))
     variant = data.draw(st.sampled_from(["vector", "bulk"]))
     check(val(rd.reduce_ex(to_dev(x, off), op, variant=variant, grid=grid)[0]), x, op)
+
+
+@pytest.mark.gpu
+@settings(max_examples=200, deadline=None, suppress_health_check=list(HealthCheck))
+@given(st.sampled_from(["float32", "float64"]), st.data())
+def test_gpu_exact_sum_arbitrary(dtype, data):
+    """The exact sum (reading R17) on arbitrary floats -- any exponent, subnormals, signed
+    zeros, inf/NaN, values that overflow any running sum -- is bit-exact against the oracle
+    through both variants, any grid and any base offset."""
+    from tests._parity import check
+    from tests.test_gpu_parity import to_dev, val
+    import paper_1710_07358_b200 as rd
+    width = 32 if dtype == "float32" else 64
+    x = data.draw(hnp.arrays(np.dtype(dtype), st.integers(0, 4000),
+                             elements=st.floats(width=width, allow_nan=True, allow_infinity=True)))
+    off = data.draw(st.integers(0, 7))
+    grid = data.draw(st.sampled_from([0, 1, 5, 300]))
+    variant = data.draw(st.sampled_from(["vector", "bulk"]))
+    check(val(rd.reduce_ex(to_dev(x, off), "sum_exact", variant=variant, grid=grid)[0]), x, "sum_exact")
