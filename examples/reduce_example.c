@@ -5,8 +5,10 @@
  *       -L/usr/local/cuda/lib64 -lcudart -o reduce_example
  *   ./reduce_example [log2n]
  *
- * Reduces n float32 ones on the GPU (sum must be n exactly for n <= 2^24)
- * and times back-to-back reduce() calls (host + device) with CUDA events. */
+ * Reduces n float32 ones on the GPU (sum must be n exactly for n <= 2^24),
+ * the paper's absorption example with the exact sum (two halves as exact
+ * records, combined), and times back-to-back reduce() calls (host + device)
+ * with CUDA events. */
 #include <cuda_runtime_api.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -41,6 +43,24 @@ int main(int argc, char** argv) {
   cudaMemcpy(&am, d_am, sizeof am, cudaMemcpyDeviceToHost);
   printf("argmax index = %lld (lowest of the ties)\n", (long long)am.index);
   if (am.index != 0) { fprintf(stderr, "wrong argmax\n"); return 1; }
+
+  /* PAPER.md P:50 fn 2: 1.5 + 4^50 - 4^50 is 0 or 1.5 by evaluation order;
+   * RD_SUM_EXACT returns the real sum, 1.5, whatever the split or order */
+  float terms[3] = {4.0f * 0x1p98f, 1.5f, -4.0f * 0x1p98f};
+  float* d_t = NULL;
+  rd_exact_record* d_rec = NULL;
+  cudaMalloc((void**)&d_t, sizeof terms);
+  cudaMalloc((void**)&d_rec, 2 * sizeof(rd_exact_record));
+  cudaMemcpy(d_t, terms, sizeof terms, cudaMemcpyHostToDevice);
+  CK(reduce_exact_partial(d_t, 1, RD_FLOAT32, d_rec, NULL));          /* block [0, 1) */
+  CK(reduce_exact_partial(d_t + 1, 2, RD_FLOAT32, d_rec + 1, NULL));  /* block [1, 3) */
+  CK(rd_combine_exact_records(d_rec, 2, RD_FLOAT32, out, NULL, NULL, NULL));
+  float e = 0.0f;
+  cudaMemcpy(&e, out, sizeof e, cudaMemcpyDeviceToHost);
+  printf("exact sum of {4^50, 1.5, -4^50} = %.1f\n", e);
+  if (e != 1.5f) { fprintf(stderr, "wrong exact sum\n"); return 1; }
+  cudaFree(d_t);
+  cudaFree(d_rec);
 
   cudaEvent_t a, b;
   cudaEventCreate(&a);
