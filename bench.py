@@ -435,6 +435,7 @@ def run_b200(args):
                        "exchange": ("fused in-kernel over NVLink (reduce_fused)" if exchange == "fused"
                                     else "NCCL all-gather + rank-order fold (reduce_multi)") if use_comm else None},
             "pct_hbm_peak": round(100 * value / (peak * ws), 2),
+            "elements_per_s": round(value * 1e9 / s, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": load_traffic(f"{dt}-{op}-2^{args.log2n}"),

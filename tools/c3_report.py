@@ -46,6 +46,41 @@ def val(t):
     return np.array([t.view(carrier).item()], dtype=np.dtype(str(carrier).replace("torch.", ""))).view(npdt)[0]
 
 
+def read_probe_gbs(nbytes=1 << 30):
+    """The same-run HBM read ceiling (tools/probe.cu; bench.py's roofline.read_probe)."""
+    import ctypes
+    lib = os.path.join(ROOT, "tools", "libprobe.so")
+    if not os.path.exists(lib):
+        return None
+    pl = ctypes.CDLL(lib)
+    pl.probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    pl.probe_occupancy.argtypes = [ctypes.c_int, ctypes.c_int]
+    x = torch.ones(nbytes // 4, dtype=torch.float32, device="cuda")
+    sink = torch.zeros(1024, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
+    best = 0.0
+    for thr, unr in ((256, 2), (1024, 2), (512, 1)):
+        blocks = 148 * max(1, pl.probe_occupancy(unr, thr)) * 4
+        for _ in range(3):
+            pl.probe_read(x.data_ptr(), nbytes, unr, blocks, thr, sink.data_ptr(), s.cuda_stream, 0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(20):
+            pl.probe_read(x.data_ptr(), nbytes, unr, blocks, thr, sink.data_ptr(), s.cuda_stream, 0)
+        b.record(s)
+        b.synchronize()
+        best = max(best, nbytes * 20 / (a.elapsed_time(b) * 1e-3) / 1e9)
+    return best
+
+
+def copy_peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--out", required=True)
@@ -53,6 +88,8 @@ def main():
     p.add_argument("--verify-max-log2n", type=int, default=28)
     args = p.parse_args()
     flush = torch.ones(128 * 2 ** 20, dtype=torch.int32, device="cuda")
+    probe, copy_peak = read_probe_gbs(), copy_peak_gbs()
+    print(json.dumps({"read_probe_gbs": probe, "copy_peak_gbs": copy_peak}), flush=True)
     rows = []
     s = torch.cuda.current_stream()
     for dtype in ("int32", "uint32", "int64", "float32", "float64"):
@@ -61,8 +98,11 @@ def main():
             n = 1 << log2n
             if n * SIZE[dtype] > 16 * 2 ** 30:
                 continue
-            for op in ops:
-                wl = inputs.default_workload(dtype, op)
+            # the exact sum twice: its default (adversarial, slow-path) workload and u01
+            cases = [(op, inputs.default_workload(dtype, op)) for op in ops]
+            if dtype.startswith("float"):
+                cases.append(("sum_exact", "u01"))
+            for op, wl in cases:
                 x = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
                 inputs.fill_device(x, wl, seed=1)
                 res, info = rd.reduce_ex(x, op)
@@ -103,6 +143,9 @@ def main():
                 row = {"dtype": dtype, "op": op, "n": n, "log2n": log2n, "workload": wl,
                        "variant": info["variant"], "grid": info["grid"], "block": info["block"],
                        "us_back_to_back": round(us, 3), "gbps_back_to_back": round(nbytes / us / 1e3, 1),
+                       "elem_per_s_back_to_back": round(n / us * 1e6, 1),
+                       "pct_read_probe": round(100 * nbytes / us / 1e3 / probe, 2) if probe else None,
+                       "pct_copy_peak": round(100 * nbytes / us / 1e3 / copy_peak, 2) if copy_peak else None,
                        "us_cold_mean5": round(sum(cold) / 5, 3),
                        "gbps_cold": round(nbytes / (sum(cold) / 5) / 1e3, 1),
                        "l2_resident": nbytes < 4 * L2, "result_ok": verdict, "err_over_tol": err_ratio}
@@ -111,7 +154,7 @@ def main():
                 del x
     with open(args.out + ".json", "w") as f:
         json.dump({"device": torch.cuda.get_device_name(), "when": time.strftime("%Y-%m-%dT%H:%M:%S"),
-                   "rows": rows}, f, indent=1)
+                   "read_probe_gbs": probe, "copy_peak_gbs": copy_peak, "rows": rows}, f, indent=1)
     with open(args.out + ".csv", "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(rows[0]))
         w.writeheader()
