@@ -331,8 +331,11 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     // from 12 MiB, 1 CTA/SM up to 48 MiB and 2 above (tools/sweep.py midops,
     // graph-captured, 7 (dtype, op): 7-16% faster at 16-64 MB; below 12 MiB
     // the cap cost up to 12%, so it does not apply there).
+    // RD_TUNE_VEC_CTAS_PER_SM (measurement only): 0 / unset = this rule, k = k CTAs
+    // per SM from 12 MiB, kNoCap = the uncapped occupancy grid.
+    constexpr uint64_t kNoCap = 1000;
     static const uint64_t kMidCap = env_u64("RD_TUNE_VEC_CTAS_PER_SM", 0);
-    if (k.variant == RD_VARIANT_VECTOR && kMidCap != 1000 && (uint64_t)n * s >= (12ull << 20)) {
+    if (k.variant == RD_VARIANT_VECTOR && kMidCap != kNoCap && (uint64_t)n * s >= (12ull << 20)) {
       const uint64_t per_sm = kMidCap ? kMidCap : ((uint64_t)n * s >= (48ull << 20) ? 2 : 1);
       const uint64_t cap = (uint64_t)di.sms * per_sm;
       if (g > cap) g = cap;
