@@ -252,14 +252,52 @@ template <int E, int L>
 struct ExState { Ex ex[E]; uint32_t flags; };
 template <typename T, int E, int L>
 __device__ __noinline__ ExState<E, L> replay_vec(ExState<E, L> st, const ExVals<L> xs, long long* w) {
+  // The full cascade a0 -> a1 -> a2 for every element, computed the same way in
+  // every lane (no data-dependent branch but the rare superaccumulator
+  // deposits): replaying lanes stay converged. (Per-element early exits made
+  // the lanes diverge per element and run this ~1-2 lanes at a time: ncu avg
+  // threads per DADD 1.5 on the adversarial `wide` workload.)
+  constexpr double kMax = 1.7976931348623157e308;
 #pragma unroll
-  for (int l = 0; l < L; ++l) ex_add<T>(st.ex[l % E], xs.v[l], w, st.flags);
+  for (int l = 0; l < L; ++l) {
+    Ex& q = st.ex[l % E];
+    const double x = xs.v[l];
+    const bool fin = fabs(x) <= kMax;                        // false for inf / NaN
+    st.flags |= fin ? (x != 0.0 ? kXNotNegZero : 0u) : ((x != x) ? kXNaN : (x > 0 ? kXPosInf : kXNegInf));
+    const double xf = fin ? x : 0.0;
+    double s, e;
+    two_sum(q.a0, xf, s, e);
+    if (__builtin_expect(!(fabs(s) <= kMax), 0)) {          // a0 + x overflows (fp64 data): deposit x
+      sacc_add<T>(w, xf);
+      s = q.a0;
+      e = 0.0;
+    }
+    q.a0 = s;
+    double s1, e1;
+    two_sum(q.a1, e, s1, e1);
+    if (__builtin_expect(!(fabs(s1) <= kMax), 0)) {
+      sacc_add<T>(w, e);
+      s1 = q.a1;
+      e1 = 0.0;
+    }
+    q.a1 = s1;
+    double s2, e2;
+    two_sum(q.a2, e1, s2, e2);
+    if (__builtin_expect(!(fabs(s2) <= kMax), 0)) {
+      sacc_add<T>(w, e1);
+      s2 = q.a2;
+      e2 = 0.0;
+    }
+    q.a2 = s2;
+    if (__builtin_expect(e2 != 0.0, 0)) sacc_add<T>(w, e2);
+  }
   return st;
 }
 
 template <typename T, int E, int L>
 __device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L], long long* w,
                                                uint32_t& flags) {
+  const unsigned mask = __activemask();
   Ex save[E];
 #pragma unroll
   for (int j = 0; j < E; ++j) save[j] = ex[j];
@@ -280,12 +318,14 @@ __device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L
       bad |= (__dsub_rn(s, q.a0) != xs[l]) | (__dsub_rn(s, xs[l]) != q.a0);
       q.a0 = s;
     }
-    if (__builtin_expect(!bad, 1)) return;
+    // warp-uniform decisions: a lane whose speculation failed takes the whole
+    // (converged) warp to the next level -- every level is exact for any data
+    if (__builtin_expect(!__any_sync(mask, bad), 1)) return;
 #pragma unroll
     for (int j = 0; j < E; ++j) ex[j] = save[j];
   }
   bad = spec2<E, L>(ex, xs);
-  if (__builtin_expect(bad, 0)) {                // replay element by element
+  if (__builtin_expect(__any_sync(mask, bad), 0)) {   // replay element by element
     ExState<E, L> st;
 #pragma unroll
     for (int j = 0; j < E; ++j) st.ex[j] = save[j];
