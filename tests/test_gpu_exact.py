@@ -179,3 +179,24 @@ def test_exact_graph_capture(rd):
         g.replay()
         torch.cuda.synchronize()
         assert bits(val(out)) == bits(want)
+
+
+def test_exact_concurrent_streams_and_mixed_ops(rd):
+    """Exact sums on concurrent streams (per-stream workspaces: slots, ticket, chunk counter),
+    interleaved with plain sums and argmax on the same streams -- every result exact."""
+    xs = [inputs.generate((1 << 21) + 7 * i, "float32" if i % 2 else "float64", "wide", seed=i + 1) for i in range(4)]
+    ds = [to_dev(x, i) for i, x in enumerate(xs)]
+    wants = [oracle.reduce(x, "sum_exact").value for x in xs]
+    streams = [torch.cuda.Stream() for _ in xs]
+    for rep in range(3):
+        outs = []
+        for d, s in zip(ds, streams):
+            with torch.cuda.stream(s):
+                rd.reduce(d, "sum")
+                outs.append(rd.reduce(d, "sum_exact"))
+                rd.reduce(d, "argmax")
+                if rep == 1:                      # the bulk variant on the same stream too
+                    outs[-1] = rd.reduce_ex(d, "sum_exact", variant="bulk")[0]
+        torch.cuda.synchronize()
+        for o, w in zip(outs, wants):
+            assert same(val(o), w)
