@@ -97,3 +97,37 @@ def test_gpu_exact_sum_arbitrary(dtype, data):
     grid = data.draw(st.sampled_from([0, 1, 5, 300]))
     variant = data.draw(st.sampled_from(["vector", "bulk"]))
     check(val(rd.reduce_ex(to_dev(x, off), "sum_exact", variant=variant, grid=grid)[0]), x, "sum_exact")
+
+
+@pytest.mark.gpu
+@settings(max_examples=120, deadline=None, suppress_health_check=list(HealthCheck))
+@given(st.sampled_from([("int32", "sum"), ("uint32", "max"), ("int64", "xor"), ("float32", "sum"),
+                        ("float64", "min"), ("float32", "argmax"), ("int64", "argmin"), ("float64", "sum_exact"),
+                        ("float32", "sum_exact")]), st.data())
+def test_gpu_random_block_splits(case, data):
+    """Any split of an array into consecutive blocks (not only rd_shard_range's), each reduced
+    to a record (exact records for the exact sum) and the records folded in block order, gives
+    the oracle's result on the whole array (the partials of consecutive blocks combine
+    in block order)."""
+    from tests._parity import check
+    from tests.test_gpu_parity import to_dev, val
+    import paper_1710_07358_b200 as rd
+    dtype, op = case
+    n = data.draw(st.integers(0, 20000))
+    if dtype.startswith("float"):
+        x = data.draw(hnp.arrays(np.dtype(dtype), n, elements=st.floats(-1e6, 1e6, width=32)))
+    else:
+        x = data.draw(hnp.arrays(np.dtype(dtype), n))
+    cuts = sorted(data.draw(st.lists(st.integers(0, n), max_size=6)))
+    bounds = list(zip([0] + cuts, cuts + [n]))
+    xd = to_dev(x, data.draw(st.integers(0, 7)))
+    exact = op == "sum_exact" and dtype.startswith("float")
+    RB = rd.EXACT_RECORD_BYTES if exact else rd.RECORD_BYTES
+    recs = torch.empty(len(bounds) * RB, dtype=torch.uint8, device="cuda")
+    for k, (b, e) in enumerate(bounds):
+        if exact:
+            rd.reduce_exact_partial(xd[b:e], rec=recs[k * RB:(k + 1) * RB])
+        else:
+            rd.reduce_partial(xd[b:e], op, rec=recs[k * RB:(k + 1) * RB])
+    got = rd.combine_exact_records(recs, dtype) if exact else rd.combine_records(recs, dtype, op)
+    check(val(got), x, op)
