@@ -102,7 +102,8 @@ typedef struct rd_arg_result {
 typedef enum {
   RD_OK = 0,
   RD_ERR_INVALID_ARG = 1,  /* NULL where a buffer is needed, unknown enum, bad config  */
-  RD_ERR_UNSUPPORTED = 2,  /* bitwise op on a float dtype                              */
+  RD_ERR_UNSUPPORTED = 2,  /* bitwise op on a float dtype; a configuration with no
+                              compiled kernel; an exact float sum into a 32-byte record */
   RD_ERR_MISALIGNED = 3,   /* base pointer not aligned to sizeof(dtype)                */
   RD_ERR_CUDA = 4,         /* CUDA launch / allocation / copy failure (rd_last_error)  */
   RD_ERR_NCCL = 5,         /* NCCL failure (rd_last_error)                             */
