@@ -289,18 +289,23 @@ const char* rd_last_error(void);
  *             F consecutive elements per work-item per iteration,
  *             bounds handled by predication instead of the (i<len)*x mask),
  *             RD_VARIANT_BULK (cp.async.bulk shared-memory ring, dynamic
- *             chunk scheduling, per-chunk partials: still deterministic)
+ *             chunk scheduling, per-chunk partials: still deterministic),
+ *             RD_VARIANT_CLUSTER (the vector kernel's body on a grid that is
+ *             one thread-block cluster of 1..16 CTAs, the CTA partials
+ *             combined over distributed shared memory: AUTO's choice for
+ *             small inputs that need 2..16 CTAs)
  *   vec_bytes 4, 8, 16 or 32 bytes per load (VECTOR variant);
  *             bytes per ring stage (BULK variant)
  *   unroll    loads in flight per thread per iteration (U; the paper's F);
  *             ring stages (BULK variant)
- *   grid      CTAs (clamped to [1, 4096])
+ *   grid      CTAs (clamped to [1, 4096]; [1, 16] for the CLUSTER variant)
  * RD_SUM_EXACT on floats has one compiled kernel per variant (vector: 32-byte
  * loads, U = 6; bulk: the default ring with 16 consumer warps): only variant
  * and grid may be chosen.
  * The chosen configuration is written to *info (may be NULL).
  * Configurations without a compiled kernel return RD_ERR_UNSUPPORTED. */
-enum { RD_VARIANT_AUTO = 0, RD_VARIANT_VECTOR = 1, RD_VARIANT_PAPER = 2, RD_VARIANT_BULK = 3 };
+enum { RD_VARIANT_AUTO = 0, RD_VARIANT_VECTOR = 1, RD_VARIANT_PAPER = 2, RD_VARIANT_BULK = 3,
+       RD_VARIANT_CLUSTER = 4 };
 typedef struct { int32_t variant, vec_bytes, unroll, block, grid, reserved[3]; } rd_config;
 typedef struct {
   int32_t variant, vec_bytes, unroll, block, grid, regs_per_thread, ctas_per_sm, reserved;

@@ -37,7 +37,7 @@ DTYPE_NAMES = {"int32": _lib.RD_INT32, "uint32": _lib.RD_UINT32, "int64": _lib.R
 RECORD_BYTES = 32
 EXACT_RECORD_BYTES = ctypes.sizeof(_lib.rd_exact_record)   # 608
 VARIANTS = {"auto": _lib.RD_VARIANT_AUTO, "vector": _lib.RD_VARIANT_VECTOR, "paper": _lib.RD_VARIANT_PAPER,
-            "bulk": _lib.RD_VARIANT_BULK}
+            "bulk": _lib.RD_VARIANT_BULK, "cluster": _lib.RD_VARIANT_CLUSTER}
 
 
 def _torch():

@@ -19,7 +19,7 @@ RD_EXACT_MAX_WORDS = 72
 RD_OK = 0
 STATUS = {0: "RD_OK", 1: "RD_ERR_INVALID_ARG", 2: "RD_ERR_UNSUPPORTED", 3: "RD_ERR_MISALIGNED",
           4: "RD_ERR_CUDA", 5: "RD_ERR_NCCL", 6: "RD_ERR_MISMATCH", 7: "RD_ERR_TIMEOUT"}
-RD_VARIANT_AUTO, RD_VARIANT_VECTOR, RD_VARIANT_PAPER, RD_VARIANT_BULK = 0, 1, 2, 3
+RD_VARIANT_AUTO, RD_VARIANT_VECTOR, RD_VARIANT_PAPER, RD_VARIANT_BULK, RD_VARIANT_CLUSTER = 0, 1, 2, 3, 4
 
 
 class rd_record(ctypes.Structure):

@@ -122,6 +122,10 @@ rd_status occupancy(int dev, const KernelRef& k, int* ctas, int* regs) {
     e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, k.smem_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)");
   }
+  if (k.variant == RD_VARIANT_CLUSTER) {   // clusters of up to 16 CTAs (non-portable size)
+    e = cudaFuncSetAttribute(k.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(NonPortableClusterSizeAllowed)");
+  }
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k.fn, k.block, k.smem_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
   cudaFuncAttributes fa;
@@ -209,7 +213,7 @@ rd_status preload_default_kernels(int dev) {
     }
     for (int op = RD_SUM; op <= RD_SUM_EXACT; ++op) {
       if (check_dtype_op(dt, op) != RD_OK) continue;
-      for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK}) {
+      for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK, RD_VARIANT_CLUSTER}) {
         KernelRef k;
         if (!lookup(dt, op, variant, 0, 0, &k)) continue;
         int occ = 0, regs = 0;
@@ -259,14 +263,21 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     set_error("block size not compiled for this variant (only the vector/paper variants' 256)");
     return RD_ERR_UNSUPPORTED;
   }
-  if (variant < RD_VARIANT_AUTO || variant > RD_VARIANT_BULK || unroll < 0 || vec_bytes < 0 ||
-      (cfg && cfg->grid < 0)) {
+  if (variant < RD_VARIANT_AUTO || variant > RD_VARIANT_CLUSTER || unroll < 0 || vec_bytes < 0 ||
+      (cfg && cfg->grid < 0) || (variant == RD_VARIANT_CLUSTER && cfg && cfg->grid > kClusterMax)) {
     set_error("bad rd_config");
     return RD_ERR_INVALID_ARG;
   }
   if (vec_bytes && vec_bytes < s && variant != RD_VARIANT_BULK) { set_error("vec_bytes < sizeof(dtype)"); return RD_ERR_INVALID_ARG; }
-  if (variant == RD_VARIANT_AUTO && unroll == 0 && vec_bytes == 0 && (uint64_t)n * s >= kBulkMinBytes)
-    variant = RD_VARIANT_BULK;   // planner: large inputs take the bulk-copy pipeline
+  if (variant == RD_VARIANT_AUTO && unroll == 0 && vec_bytes == 0) {
+    const uint64_t bytes = (uint64_t)n * s;
+    if (bytes >= kBulkMinBytes) {
+      variant = RD_VARIANT_BULK;      // planner: large inputs take the bulk-copy pipeline
+    } else if (bytes > (uint64_t)kBlock * kDefaultUnroll4 * kDefaultVec && bytes <= kClusterMaxBytes &&
+               !(cfg && cfg->grid > kClusterMax)) {
+      variant = RD_VARIANT_CLUSTER;   // 2..16 CTAs: one cluster, combine over DSMEM
+    }
+  }
   KernelRef k;
   if (!lookup(dtype, op, variant, unroll, vec_bytes, &k)) {
     set_error("no compiled kernel for this (dtype, op, variant, unroll, vec_bytes)");
@@ -288,7 +299,7 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   a.x = (const unsigned char*)x;
   a.n = n;
   uint64_t g = (uint64_t)di.sms * occ;   // persistent grid
-  if (k.variant == RD_VARIANT_VECTOR || k.variant == RD_VARIANT_BULK) {
+  if (k.variant == RD_VARIANT_VECTOR || k.variant == RD_VARIANT_BULK || k.variant == RD_VARIANT_CLUSTER) {
     const int vb = k.variant == RD_VARIANT_BULK ? 16 : k.vec_bytes;   // body alignment
     const uint64_t L = (uint64_t)(vb / s);
     const uint64_t mis = (uint64_t)((uintptr_t)x % (uintptr_t)vb);
@@ -321,8 +332,9 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   } else {
     // work units handed out by the grid-stride loop; fewer CTAs than one
     // resident wave when there is less work than one unrolled pass
-    const uint64_t units = k.variant == RD_VARIANT_VECTOR ? a.nvec : (n + k.unroll - 1) / k.unroll;
-    const uint64_t per_cta = (uint64_t)k.block * (k.variant == RD_VARIANT_VECTOR ? k.unroll : 1);
+    const bool vec = k.variant == RD_VARIANT_VECTOR || k.variant == RD_VARIANT_CLUSTER;
+    const uint64_t units = vec ? a.nvec : (n + k.unroll - 1) / k.unroll;
+    const uint64_t per_cta = (uint64_t)k.block * (vec ? k.unroll : 1);
     uint64_t need = (units + per_cta - 1) / per_cta;
     if (need < 1) need = 1;
     if (g > need) g = need;
@@ -343,6 +355,7 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   }
   if (cfg && cfg->grid > 0) g = (uint64_t)cfg->grid;
   if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
+  if (k.variant == RD_VARIANT_CLUSTER && g > (uint64_t)kClusterMax) g = kClusterMax;
   if (g < 1) g = 1;
 
   a.out = out;
@@ -368,11 +381,18 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   lc.blockDim = dim3((unsigned)k.block);
   lc.dynamicSmemBytes = (size_t)k.smem_bytes;
   lc.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
+  if (k.variant == RD_VARIANT_CLUSTER) {   // the whole grid is one cluster
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)g;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    lc.numAttrs = 2;
+  }
   e = cudaLaunchKernelEx(&lc, k.fn, a);
   if (e != cudaSuccess) return cuda_fail(e, "reduce kernel launch");
   if (info) {

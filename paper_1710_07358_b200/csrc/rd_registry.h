@@ -69,6 +69,13 @@ constexpr int kBulkStageBytes = 32768;
 // AUTO picks the bulk pipeline at or above this many input bytes (below it the
 // vector kernel's shorter latency chain wins).
 constexpr uint64_t kBulkMinBytes = 128ull << 20;
+// AUTO picks the one-cluster kernel (at most kClusterMax = 16 CTAs, a
+// non-portable cluster size allowed on sm_100) for 32 KB < n*s <= 1 MiB: up to
+// 512 KB the vector plan needs 2..16 CTAs anyway; at 512 KB - 1 MiB 16 CTAs
+// doing two passes still beat 32 ticketed CTAs (graph-captured float32 Σ
+// 2^18: 2.85 vs 3.11 us; at 2 MiB they lose: 3.42 vs 3.21; tools/gpu/cl_probe.py).
+constexpr int kClusterMax = 16;
+constexpr uint64_t kClusterMaxBytes = 1ull << 20;
 
 // Helpers used by the instantiation units: the default kernels of one (dtype, op).
 template <class OpT>
@@ -78,6 +85,11 @@ inline bool lookup_default(int variant, int unroll, int vec_bytes, KernelRef* r)
   if (variant == RD_VARIANT_BULK) {
     return bulk_entry<OpT, kBulkStages, kBulkStageBytes>(unroll ? unroll : kBulkStages,
                                                          vec_bytes ? vec_bytes : kBulkStageBytes, r);
+  }
+  if (variant == RD_VARIANT_CLUSTER) {
+    if ((unroll && unroll != du) || (vec_bytes && vec_bytes != kDefaultVec)) return false;
+    *r = KernelRef{rd_cluster_kernel<OpT, kBlock, du, kDefaultVec>, kBlock, du, kDefaultVec, RD_VARIANT_CLUSTER};
+    return true;
   }
   if (variant != RD_VARIANT_AUTO && variant != RD_VARIANT_VECTOR) return false;
   const int u = unroll ? unroll : du;

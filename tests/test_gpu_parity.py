@@ -737,3 +737,78 @@ def test_host_threads_concurrently(rd):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+# ------------------------------------------------------------------ cluster variant (small inputs)
+@pytest.mark.parametrize("dtype,op", [("float32", "sum"), ("int32", "sum"), ("float64", "prod"), ("uint32", "min"),
+                                      ("int64", "xor"), ("float32", "argmin"), ("float64", "argmax"),
+                                      ("float32", "max"), ("float64", "sum_compensated"), ("int32", "argmax")])
+def test_cluster_variant(rd, dtype, op):
+    """The one-cluster kernel (2..16 CTAs combined over DSMEM): every forced grid size 1..16,
+    misaligned bases, and AUTO's choice at 32 KB < n*s <= 512 KB."""
+    wl = inputs.default_workload(dtype, op)
+    s = np.dtype(dtype).itemsize
+    for n in (1, 9, 4099, (1 << 15) // s + 1, (1 << 17) // s + 5, (1 << 19) // s, (1 << 20) // s - 3):
+        x = inputs.generate(n, dtype, wl, seed=n % 5 + 1)
+        for off in (0, 3):
+            xd = to_dev(x, off)
+            for g in (1, 2, 3, 8, 13, 16):
+                out, info = rd.reduce_ex(xd, op, variant="cluster", grid=g)
+                assert info["variant"] == "cluster" and info["grid"] == g
+                _parity.check(val(out), x, op)
+            out, info = rd.reduce_ex(xd, op)
+            if (1 << 15) < n * s <= (1 << 20):
+                assert info["variant"] == "cluster" and 1 <= info["grid"] <= 16, info
+            _parity.check(val(out), x, op)
+    with pytest.raises(rd.ReduceError):
+        rd.reduce_ex(to_dev(inputs.generate(1000, dtype, wl)), op, variant="cluster", grid=17)
+
+
+def test_cluster_variant_records_graph_and_fused(rd):
+    """The cluster kernel writing records, captured in a CUDA graph, and inside the fused
+    exchange (virtual ranks)."""
+    n = (1 << 17) + 11                                # 512 KB of float32 -> AUTO: cluster
+    x = inputs.generate(n, "float32", "u01", seed=4)
+    xd = to_dev(x, 1)
+    assert rd.reduce_ex(xd, "sum")[1]["variant"] == "cluster"
+    recs = torch.empty(4 * 32, dtype=torch.uint8, device="cuda")
+    for r in range(4):
+        b, c = rd.shard_range(n, 4, r)
+        rd.reduce_partial(xd[b:b + c], "sum", rec=recs[r * 32:(r + 1) * 32])
+    _parity.check(val(rd.combine_records(recs, "float32", "sum")), x, "sum")
+    out = torch.empty((), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        rd.reduce(xd, "sum", out=out)
+    torch.cuda.synchronize()
+    want = val(out)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        rd.reduce(xd, "sum", out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert val(out).tobytes() == want.tobytes()
+    W = 3
+    comms = rd.FusedComm.local(W, torch.cuda.current_device())
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    try:
+        for op in ("sum", "argmax", "xor"):
+            dt = "int32" if op == "xor" else "float32"
+            xx = inputs.generate(3 * (1 << 16) + 7, dt, inputs.default_workload(dt, op), seed=2)
+            xdd = to_dev(xx)
+            outs = []
+            for r in range(W):
+                b, c = rd.shard_range(xx.size, W, r)
+                with torch.cuda.stream(streams[r]):
+                    outs.append(comms[r].reduce(xdd[b:b + c], op))
+            torch.cuda.synchronize()
+            for r in range(W):
+                comms[r].check(streams[r])
+            vals = [val(o) for o in outs]
+            assert all(repr(v) == repr(vals[0]) for v in vals)
+            _parity.check(vals[0], xx, op)
+    finally:
+        torch.cuda.synchronize()
+        for c in comms:
+            c.destroy()

@@ -47,7 +47,40 @@ def run(path, x_by_dtype):
     return res
 
 
+def run_small(path):
+    """graph-captured us per launch at small n (float32 sum), 100 launches per replay"""
+    L = ctypes.CDLL(path)
+    L.reduce.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    out = torch.empty(2, dtype=torch.int64, device="cuda")
+    res = {}
+    for log2n in (10, 12, 13, 14, 16, 18):
+        x = torch.rand(1 << log2n, device="cuda")
+        gs = torch.cuda.Stream()
+        with torch.cuda.stream(gs):
+            L.reduce(x.data_ptr(), x.numel(), 3, 0, out.data_ptr(), gs.cuda_stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            for _ in range(100):
+                L.reduce(x.data_ptr(), x.numel(), 3, 0, out.data_ptr(), gs.cuda_stream)
+        ts = []
+        for _ in range(7):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 10.0)
+        ts.sort()
+        res[f"2^{log2n}"] = round(ts[3], 3)
+    return res
+
+
 if __name__ == "__main__":
+    if "--small" in sys.argv:
+        for p in [a for a in sys.argv[1:] if a != "--small"]:
+            print(json.dumps({"lib": os.path.basename(p), **run_small(p)}), flush=True)
+        sys.exit(0)
     n = 1 << 28
     xs = {}
     for dtype in ("float32", "int32", "float64"):
