@@ -4,7 +4,7 @@ synccheck, initcheck) runs on one GPU:
 
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 
-Covers both kernel variants (vector, bulk), the paper-listing variant, every
+Covers the kernel variants (vector, bulk, cluster), the paper-listing variant, every
 (dtype, op) pair, misaligned bases, forced multi-CTA grids (ticket path), arg
 ops, records + rd_combine_records, exact records, and reduce_host. Exits non-zero if a result
 disagrees with the oracle."""
@@ -53,7 +53,8 @@ def main():
             for n, off in ((0, 0), (5, 1), (1000, 3), (70001, 2)):
                 x = inputs.generate(n, dtype, wl, seed=3)
                 xd = dev(x, off)
-                for variant, grid in (("vector", 0), ("vector", 7), ("bulk", 0), ("bulk", 3)):
+                for variant, grid in (("vector", 0), ("vector", 7), ("bulk", 0), ("bulk", 3), ("cluster", 0),
+                                      ("cluster", 5)):
                     out, _ = rd.reduce_ex(xd, op, variant=variant, grid=grid)
                     _parity.check(val(out), x, op)
                     count += 1
