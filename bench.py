@@ -161,12 +161,25 @@ def run_reference(args):
         "config": {"workload": f"{dt} {op}, n=2^{args.log2n} per GPU (u01, seed 1); "
                                f"each reference step folds the first {m} elements (bounded sample)",
                    "n_per_gpu": n_full, "op": op, "sample_elements": m},
-        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"first {m} of {n_full} elements per step, {args.steps} steps"},
         "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
     return 0
+
+
+def cpu_model() -> str:
+    """The host CPU's model name (the report records it beside the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 # ====================================================================== B200 arm
@@ -405,7 +418,7 @@ def run_b200(args):
                 if el > args.cpu_seconds or passes >= 50:
                     break
             cpu = {"value": round(gbps(m * s * passes, el), 4), "unit": "GB/s", "cores": 1,
-                   "kind": "oracle",
+                   "kind": "oracle", "cpu_model": cpu_model(),
                    "sample": f"{passes} full pass(es) over the same {n}-element host array "
                              f"({el:.1f} s, single thread, gcc -O2)"}
             # all host cores: the same plain fold on contiguous chunks (ctypes drops
