@@ -299,9 +299,9 @@ const char* rd_last_error(void);
  *   unroll    loads in flight per thread per iteration (U; the paper's F);
  *             ring stages (BULK variant)
  *   grid      CTAs (clamped to [1, 4096]; [1, 16] for the CLUSTER variant)
- * RD_SUM_EXACT on floats has one compiled kernel per variant (vector: 32-byte
- * loads, U = 6; bulk: the default ring with 16 consumer warps): only variant
- * and grid may be chosen.
+ * RD_SUM_EXACT on floats has one compiled kernel per variant (vector and
+ * cluster: 32-byte loads, U = 6; bulk: the default ring with 16 consumer
+ * warps): only variant and grid may be chosen.
  * The chosen configuration is written to *info (may be NULL).
  * Configurations without a compiled kernel return RD_ERR_UNSUPPORTED. */
 enum { RD_VARIANT_AUTO = 0, RD_VARIANT_VECTOR = 1, RD_VARIANT_PAPER = 2, RD_VARIANT_BULK = 3,

@@ -202,7 +202,7 @@ bool plan_bulk(uint64_t body_bytes, uint64_t stage_bytes, BulkPlan* p, bool inde
 rd_status preload_default_kernels(int dev) {
   for (int dt = RD_INT32; dt <= RD_FLOAT64; ++dt) {
     if (dt == RD_FLOAT32 || dt == RD_FLOAT64) {     // the exact-sum kernels (fused mode 2 too)
-      for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK}) {
+      for (int variant : {RD_VARIANT_VECTOR, RD_VARIANT_BULK, RD_VARIANT_CLUSTER}) {
         ExactRef x;
         if (!lookup_exact(dt, variant, &x)) continue;
         int occ = 0, regs = 0;
@@ -429,11 +429,21 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   if (mode == 1 && (uintptr_t)xrec % 8 != 0) { set_error("rec is not 8-byte aligned"); return RD_ERR_MISALIGNED; }
   if (n >= (1ull << 40)) { set_error("n >= 2^40"); return RD_ERR_INVALID_ARG; }
   int variant = cfg ? cfg->variant : RD_VARIANT_AUTO;
-  if (variant != RD_VARIANT_AUTO && variant != RD_VARIANT_VECTOR && variant != RD_VARIANT_BULK) {
-    set_error("RD_SUM_EXACT: variant must be auto, vector or bulk");
+  if (variant != RD_VARIANT_AUTO && variant != RD_VARIANT_VECTOR && variant != RD_VARIANT_BULK &&
+      variant != RD_VARIANT_CLUSTER) {
+    set_error("RD_SUM_EXACT: variant must be auto, vector, bulk or cluster");
     return RD_ERR_UNSUPPORTED;
   }
-  if (variant == RD_VARIANT_AUTO) variant = (uint64_t)n * s >= kBulkMinBytes ? RD_VARIANT_BULK : RD_VARIANT_VECTOR;
+  if (variant == RD_VARIANT_CLUSTER && cfg && cfg->grid > kClusterMax) {
+    set_error("cluster variant: grid <= 16");
+    return RD_ERR_INVALID_ARG;
+  }
+  if (variant == RD_VARIANT_AUTO) {
+    const uint64_t bytes = (uint64_t)n * s;
+    variant = bytes >= kBulkMinBytes ? RD_VARIANT_BULK
+              : (bytes > (uint64_t)kBlock * kExactUnroll * 32 && bytes <= kClusterMaxBytes &&
+                 !(cfg && cfg->grid > kClusterMax)) ? RD_VARIANT_CLUSTER : RD_VARIANT_VECTOR;
+  }
   ExactRef k;
   if (!lookup_exact(dtype, variant, &k)) { set_error("no compiled exact-sum kernel (RD_TUNE_EXACT?)"); return RD_ERR_UNSUPPORTED; }
   if (cfg && ((cfg->unroll && cfg->unroll != k.unroll) || (cfg->vec_bytes && cfg->vec_bytes != k.vec_bytes) ||
@@ -487,6 +497,7 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   }
   if (cfg && cfg->grid > 0) g = (uint64_t)cfg->grid;
   if (g > (uint64_t)kMaxGrid) g = kMaxGrid;
+  if (k.variant == RD_VARIANT_CLUSTER && g > (uint64_t)kClusterMax) g = kClusterMax;
   a.out = out;
   a.rec = xrec;
   a.partials = ws.xpart;
@@ -507,11 +518,18 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
   lc.blockDim = dim3((unsigned)k.block);
   lc.dynamicSmemBytes = (size_t)k.smem_bytes;
   lc.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
+  if (k.variant == RD_VARIANT_CLUSTER) {   // the whole grid is one cluster
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = (unsigned)g;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    lc.numAttrs = 2;
+  }
   e = cudaLaunchKernelEx(&lc, k.fn, a);
   if (e != cudaSuccess) return cuda_fail(e, "exact-sum kernel launch");
   if (info) {

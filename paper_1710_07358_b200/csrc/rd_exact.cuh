@@ -534,12 +534,12 @@ __device__ __forceinline__ void sacc_flush_warp(long long* w, const double (&d)[
   __syncwarp();
 }
 
-// a3-a7, shared by both exact kernels: expansions -> warp superaccumulators
-// -> the CTA's slot -> (last CTA) the sum of the G slots, rounded once.
+// a3-a5, shared by the exact kernels: the expansions -> warp
+// superaccumulators -> the CTA's carried-digit sums in cta[0..NW) (< 2^35 per
+// word) and its flags in cta[NW]. Ends with __syncthreads.
 template <typename T, int B, int E>
-__device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
-                                             long long* tot, unsigned& s_flags, unsigned& s_last,
-                                             const XArgs& args) {
+__device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
+                                                unsigned& s_flags, long long* cta) {
   constexpr int NW = ExactTraits<T>::kWords;
   constexpr int NWARP = B / 32;
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -564,15 +564,53 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
   // a4: each warp carries its words into digits
   if (ln == 0) sacc_normalise<NW>(w);
   __syncthreads();
-  // a5: the CTA's words (sum of NWARP digit vectors: < 2^35 per word)
-  long long* slot = args.partials + (size_t)blockIdx.x * (NW + 1);
+  // a5: the CTA's words (sum of NWARP digit vectors)
   if (threadIdx.x < NW) {
     long long s = 0;
 #pragma unroll
     for (int q = 0; q < NWARP; ++q) s += sacc[q][threadIdx.x];
-    __stcg(slot + threadIdx.x, s);
+    cta[threadIdx.x] = s;
   }
-  if (threadIdx.x == NW) __stcg(slot + NW, (long long)s_flags);
+  if (threadIdx.x == NW) cta[NW] = (long long)s_flags;
+  __syncthreads();
+}
+
+// a7: the carried total (words, normalised) -> the result (mode 0, thread 0),
+// an exact record (mode 1, thread 0) or the fused exchange (mode 2, warp 0)
+template <typename T>
+__device__ __forceinline__ void exact_emit(long long* words, unsigned flags, const XArgs& args) {
+  constexpr int NW = ExactTraits<T>::kWords;
+  if (threadIdx.x == 0) {
+    if (args.mode == 0) {
+      exact_store<T>(words, flags, args.n, args.out);
+    } else if (args.mode == 1) {
+      rd_exact_record* r = args.rec;
+      r->tag = args.tag;
+      r->status = 0;
+      r->n = args.n;
+      r->flags = flags;
+      r->nwords = NW;
+      r->reserved = 0;
+      for (int k = 0; k < NW; ++k) r->word[k] = words[k];
+      for (int k = NW; k < RD_EXACT_MAX_WORDS; ++k) r->word[k] = 0;
+    }
+  }
+  if (args.mode == 2 && threadIdx.x < 32) {
+    __syncwarp();
+    exact_fused_exchange<T>(words, flags, args);
+  }
+}
+
+// a3-a7 for the persistent grids: the CTA's words go to workspace slot
+// blockIdx; the last CTA (atomic ticket) adds the G slots and emits.
+template <typename T, int B, int E>
+__device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
+                                             long long* tot, unsigned& s_flags, unsigned& s_last,
+                                             const XArgs& args) {
+  constexpr int NW = ExactTraits<T>::kWords;
+  long long* slot = args.partials + (size_t)blockIdx.x * (NW + 1);
+  exact_cta_words<T, B, E>(ex, flags, sacc, s_flags, tot);
+  if (threadIdx.x <= NW) __stcg(slot + threadIdx.x, tot[threadIdx.x]);
   // a6: last CTA adds the G slots
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -610,60 +648,70 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
     sacc_normalise<NW>(sacc[0]);
     *args.ticket = 0u;
     if (args.work) *args.work = 0u;
-    if (args.mode == 0) {
-      exact_store<T>(sacc[0], s_flags, args.n, args.out);
-    } else if (args.mode == 1) {
-      rd_exact_record* r = args.rec;
-      r->tag = args.tag;
-      r->status = 0;
-      r->n = args.n;
-      r->flags = s_flags;
-      r->nwords = NW;
-      r->reserved = 0;
-      for (int k = 0; k < NW; ++k) r->word[k] = sacc[0][k];
-      for (int k = NW; k < RD_EXACT_MAX_WORDS; ++k) r->word[k] = 0;
+  }
+  __syncthreads();
+  exact_emit<T>(sacc[0], s_flags, args);
+}
+
+// a6-a7 when the grid is one thread-block cluster (small inputs): rank 0 adds
+// the G CTAs' words over distributed shared memory -- no slot, fence or ticket.
+__device__ __forceinline__ long long dsmem_load_i64(const long long* local, unsigned rank) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(local);
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(a), "r"(rank));
+  long long v;
+  asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+template <typename T, int B, int E>
+__device__ __forceinline__ void exact_finish_cluster(Ex (&ex)[E], uint32_t flags,
+                                                     long long (*sacc)[ExactTraits<T>::kWords], long long* cta,
+                                                     unsigned& s_flags, const XArgs& args) {
+  constexpr int NW = ExactTraits<T>::kWords;
+  exact_cta_words<T, B, E>(ex, flags, sacc, s_flags, cta);
+  cluster_sync();
+  if (cluster_ctarank() == 0) {
+    const unsigned G = cluster_nctarank();
+    if (threadIdx.x <= NW) {
+      const int j = threadIdx.x;
+      long long s = 0;
+      for (unsigned r = 0; r < G; ++r) {
+        const long long v = dsmem_load_i64(cta + j, r);
+        s = (j == NW) ? (s | v) : (s + v);
+      }
+      if (j < NW) sacc[0][j] = s;
+      else s_flags = (unsigned)s;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) sacc_normalise<NW>(sacc[0]);
+    __syncthreads();
+    exact_emit<T>(sacc[0], s_flags, args);
   }
-  if (args.mode == 2 && threadIdx.x < 32) {
-    __syncwarp();
-    exact_fused_exchange<T>(sacc[0], s_flags, args);
-  }
+  cluster_sync();   // the other CTAs' words stay alive until rank 0 has read them
 }
 
 // --------------------------------------------------------------------- kernel
-template <typename T, int B, int U, int E, int MINB>
-__global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const __grid_constant__ XArgs args) {
-  using TR = ExactTraits<T>;
-  constexpr int NW = TR::kWords;
+// The exact vector kernels' streaming part (a1, a2): every thread's E
+// expansions over its grid-stride share of 32-byte vectors, and the head/tail
+// stragglers. The main loop's trip count is warp-uniform (tested on the warp's
+// last lane, whose index is the largest), so every iteration can end with a
+// __syncwarp: a lane that replayed a vector (divergent) rejoins its warp
+// there. Without it the warp stayed split after the first divergent replay
+// and ran the loop ~2 lanes at a time (ncu: 2.0 avg threads per F2F).
+template <typename T, int B, int U, int E>
+__device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E], long long* w, uint32_t& flags) {
   constexpr int VB = 32;
   constexpr int L = VB / (int)sizeof(T);
-  constexpr int NWARP = B / 32;
-  __shared__ long long sacc[NWARP][NW];
-  __shared__ long long tot[B];
-  __shared__ unsigned s_flags, s_last;
-
-  const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
-  if (threadIdx.x == 0) s_flags = 0;
-  __syncthreads();
-  long long* w = sacc[warp];
-
-  Ex ex[E];
+  const int ln = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < E; ++j) ex[j] = Ex{-0.0, -0.0, -0.0};
-  uint32_t flags = 0;
-
   const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * B;
   const unsigned char* body = args.x + args.head * sizeof(T);
   pdl_wait();
   const uint64_t nvec = args.nvec;
   uint64_t i = tid;
-  // The main loop's trip count is warp-uniform (tested on the warp's last
-  // lane, whose index is the largest), so every iteration can end with a
-  // __syncwarp: a lane that replayed a vector (divergent) rejoins its warp
-  // there. Without it the warp stayed split after the first divergent replay
-  // and ran the loop ~2 lanes at a time (ncu: 2.0 avg threads per F2F).
   const uint64_t lag = 31 - (uint64_t)ln;        // lane 31's index = i + lag
   for (; i + lag + (uint64_t)(U - 1) * stride < nvec; i += (uint64_t)U * stride) {
     Vec<VB> v[U];
@@ -688,8 +736,43 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const __grid_constant
   pdl_trigger();
   // a2: head and tail stragglers
   if (tid < args.head) ex_add<T>(ex[0], widen(ldg_scalar<T>(args.x + tid * sizeof(T))), w, flags);
-  if (tid < args.tail) ex_add<T>(ex[1], widen(ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T))), w, flags);
+  if (tid < args.tail) ex_add<T>(ex[E - 1], widen(ldg_scalar<T>(args.x + (args.tail_start + tid) * sizeof(T))), w, flags);
+}
+
+// The persistent vector form: grid-stride, then slots + the atomic ticket.
+template <typename T, int B, int U, int E, int MINB>
+__global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const __grid_constant__ XArgs args) {
+  constexpr int NW = ExactTraits<T>::kWords;
+  constexpr int NWARP = B / 32;
+  __shared__ long long sacc[NWARP][NW];
+  __shared__ long long tot[B];
+  __shared__ unsigned s_flags, s_last;
+  for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_flags = 0;
+  __syncthreads();
+  Ex ex[E];
+  uint32_t flags = 0;
+  exact_vector_body<T, B, U, E>(args, ex, sacc[threadIdx.x >> 5], flags);
   exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
+}
+
+// The same on a grid that is ONE thread-block cluster (<= 16 CTAs): AUTO's
+// choice for small inputs (n*s <= 1 MiB), like rd_cluster_kernel -- the CTA
+// words are added over distributed shared memory (no slots, fence or ticket).
+template <typename T, int B, int U, int E, int MINB>
+__global__ void __launch_bounds__(B, MINB) rd_exact_cluster_kernel(const __grid_constant__ XArgs args) {
+  constexpr int NW = ExactTraits<T>::kWords;
+  constexpr int NWARP = B / 32;
+  __shared__ long long sacc[NWARP][NW];
+  __shared__ long long cta[NW + 1];
+  __shared__ unsigned s_flags;
+  for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
+  if (threadIdx.x == 0) s_flags = 0;
+  __syncthreads();
+  Ex ex[E];
+  uint32_t flags = 0;
+  exact_vector_body<T, B, U, E>(args, ex, sacc[threadIdx.x >> 5], flags);
+  exact_finish_cluster<T, B, E>(ex, flags, sacc, cta, s_flags, args);
 }
 
 // The bulk-copy form (like rd_bulk_kernel): one producer lane streams

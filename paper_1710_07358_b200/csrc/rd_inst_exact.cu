@@ -50,6 +50,19 @@ static bool pick_bulk(ExactRef* r) {
 }
 
 bool lookup_exact(int dtype, int variant, ExactRef* r) {
+  if (variant == RD_VARIANT_CLUSTER) {
+    if (dtype == RD_FLOAT32) {
+      *r = ExactRef{rd_exact_cluster_kernel<float, kBlock, kExactUnroll, kExactExpansions, kExactMinBlocks>, kBlock,
+                    kExactUnroll, 32, RD_VARIANT_CLUSTER};
+      return true;
+    }
+    if (dtype == RD_FLOAT64) {
+      *r = ExactRef{rd_exact_cluster_kernel<double, kBlock, kExactUnroll, kExactExpansions, kExactMinBlocks>, kBlock,
+                    kExactUnroll, 32, RD_VARIANT_CLUSTER};
+      return true;
+    }
+    return false;
+  }
   if (variant == RD_VARIANT_BULK) {
     if (dtype == RD_FLOAT32) return pick_bulk<float>(r);
     if (dtype == RD_FLOAT64) return pick_bulk<double>(r);

@@ -58,8 +58,8 @@ def test_exact_offsets_grids_and_shards(rd, dtype):
         assert same(val(rd.reduce(xd, "sum_exact")), want), off
         assert same(val(rd.reduce_ex(xd, "sum_exact", variant="bulk")[0]), want), off
     xd = to_dev(x, 3)
-    for variant in ("vector", "bulk"):
-        for grid in (1, 2, 3, 7, 148, 296, 1000, 4096):
+    for variant in ("vector", "bulk", "cluster"):
+        for grid in ((1, 2, 3, 7, 16) if variant == "cluster" else (1, 2, 3, 7, 148, 296, 1000, 4096)):
             got, info = rd.reduce_ex(xd, "sum_exact", variant=variant, grid=grid)
             assert info["grid"] == grid and info["variant"] == variant and same(val(got), want), (variant, grid)
     RB = rd.EXACT_RECORD_BYTES
@@ -200,3 +200,40 @@ def test_exact_concurrent_streams_and_mixed_ops(rd):
         torch.cuda.synchronize()
         for o, w in zip(outs, wants):
             assert same(val(o), w)
+
+
+@pytest.mark.parametrize("dtype", FLT)
+def test_exact_cluster_small_sizes(rd, dtype):
+    """AUTO's one-cluster exact kernel at 48 KB < n*s <= 1 MiB (every grid 1..16 forced too),
+    as a record, and through the fused exchange."""
+    s = np.dtype(dtype).itemsize
+    for n in ((1 << 16) // s + 3, (1 << 18) // s + 1, (1 << 20) // s):
+        x = inputs.generate(n, dtype, "wide", seed=n % 7 + 1)
+        want = oracle.reduce(x, "sum_exact").value
+        xd = to_dev(x, 5)
+        got, info = rd.reduce_ex(xd, "sum_exact")
+        assert info["variant"] == "cluster" and same(val(got), want)
+        for g in range(1, 17, 3):
+            assert same(val(rd.reduce_ex(xd, "sum_exact", variant="cluster", grid=g)[0]), want)
+        rec = rd.reduce_exact_partial(xd)
+        assert same(val(rd.combine_exact_records(rec, dtype)), want)
+    comms = rd.FusedComm.local(2, torch.cuda.current_device())
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    try:
+        n = (1 << 19) // s + 9
+        x = inputs.generate(n, dtype, "wide", seed=3)
+        xd = to_dev(x)
+        outs = []
+        for r in range(2):
+            b, c = rd.shard_range(n, 2, r)
+            with torch.cuda.stream(streams[r]):
+                outs.append(comms[r].reduce(xd[b:b + c], "sum_exact"))
+        torch.cuda.synchronize()
+        for r in range(2):
+            comms[r].check(streams[r])
+        want = oracle.reduce(x, "sum_exact").value
+        assert all(same(val(o), want) for o in outs)
+    finally:
+        torch.cuda.synchronize()
+        for c in comms:
+            c.destroy()

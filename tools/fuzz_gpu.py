@@ -76,8 +76,6 @@ def main():
         x, wl = draw_input(rng, dtype, op, n)
         off = int(rng.integers(0, 8))
         variant = ["auto", "vector", "bulk", "cluster"][int(rng.integers(0, 4))]
-        if variant == "cluster" and op == "sum_exact" and dtype in FLT:
-            variant = "vector"
         grid = 0 if rng.random() < 0.5 else int(rng.integers(1, 17 if variant == "cluster" else 600))
         try:
             out, info = rd.reduce_ex(dev(x, off), op, variant=variant, grid=grid)

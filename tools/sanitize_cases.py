@@ -55,8 +55,6 @@ def main():
                 xd = dev(x, off)
                 for variant, grid in (("vector", 0), ("vector", 7), ("bulk", 0), ("bulk", 3), ("cluster", 0),
                                       ("cluster", 5)):
-                    if variant == "cluster" and op == "sum_exact" and dtype.startswith("float"):
-                        continue      # the exact float sum has its own kernels (vector / bulk)
                     out, _ = rd.reduce_ex(xd, op, variant=variant, grid=grid)
                     _parity.check(val(out), x, op)
                     count += 1
