@@ -5,7 +5,8 @@
 // the exact sum is the one result no order, grid, variant, base alignment or
 // GPU count can change -- so it is bitwise reproducible by construction.
 //
-// Design (one single-pass launch; a vector-load and a bulk-copy form):
+// Design (one single-pass launch; a vector-load form, its one-cluster form
+// for small inputs, and a bulk-copy form):
 //  a1  each thread streams vectors (32-byte loads, or LDS.128 from the bulk
 //      ring) and adds every element (fp32 widened to fp64, exactly) into one
 //      of E three-term expansions (a0, a1, a2), a0 + a1 + a2 exact. Per
@@ -26,7 +27,7 @@
 //      adds its warps' digits.
 //  a6  the CTA's words go to workspace slot blockIdx; the last CTA (atomic
 //      ticket) adds the G slots word by word (integers: any order is exact),
-//      carries, and
+//      carries (one-cluster form: rank 0 adds the CTAs' words over DSMEM), and
 //  a7  rounds once: the 64 bits below the leading one give the p kept bits,
 //      the guard bit and (with every lower digit) the sticky bit; ties to even;
 //      the float is assembled as (shift << (p-1)) + q, which carries a rounded-
