@@ -16,7 +16,7 @@ import inputs  # noqa: E402
 DT = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
 OPS = {"sum": 0, "max": 3, "argmin": 7, "argmax": 8, "sum_exact": 10}
 PAIRS = [("float32", "argmin"), ("float32", "argmax"), ("int32", "argmax"), ("float64", "argmin"),
-         ("float32", "sum"), ("int32", "sum"), ("float64", "max")]
+         ("float32", "sum"), ("int32", "sum"), ("float64", "max"), ("int64", "argmin"), ("uint32", "argmax")]
 if os.environ.get("AB_EXACT"):
     PAIRS.append(("float32", "sum_exact"))
 
@@ -83,7 +83,7 @@ if __name__ == "__main__":
         sys.exit(0)
     n = 1 << 28
     xs = {}
-    for dtype in ("float32", "int32", "float64"):
+    for dtype in ("float32", "int32", "float64", "int64", "uint32"):
         xs[dtype] = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
         inputs.fill_device(xs[dtype], "u01" if dtype.startswith("float") else "int_small", seed=1)
     for rnd in range(2):                      # interleaved twice: clock drift shows up
