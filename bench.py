@@ -208,7 +208,9 @@ def run_b200(args):
     wl = "u01" if dt.startswith("float") else inputs.default_workload(dt, op)
     x = torch.empty(n, dtype=getattr(torch, dt), device=dev)
     inputs.fill_device(x, wl, seed=1, offset=rank * n, n_total=n * ws)
-    out = torch.empty((), dtype=x.dtype, device=dev)
+    # one element, or a 16-byte rd_arg_result for argmin / argmax
+    out = torch.empty(2, dtype=torch.int64, device=dev) if op in rd.ARG_OPS else \
+        torch.empty((), dtype=x.dtype, device=dev)
     comm = rd.Comm.from_process_group() if use_comm else None   # NCCL all-gather exchange
     exchange = "nccl"
     if use_comm and args.exchange == "fused":
@@ -309,7 +311,7 @@ def run_b200(args):
     achieved = gbps(n * s, kern_ms / 1e3)
 
     # check the timed result once (cheap property: finite, plausible)
-    res = out.item()
+    res = int(out[1].item()) if op in rd.ARG_OPS else out.item()   # arg ops: the index
 
     # ---------------- e2e: host (pinned) -> device -> result -> host, through the public API
     ke = 0 if args.profile else max(3, min(K, 10))
@@ -332,7 +334,7 @@ def run_b200(args):
         for _ in range(ke):
             x.copy_(host, non_blocking=True)
             comm.reduce(x, op, out=out)
-            out.item()
+            out.cpu()
         te = time.perf_counter() - te
         import torch.distributed as dist
         tt = torch.tensor([te], device=dev, dtype=torch.float64)
@@ -340,7 +342,7 @@ def run_b200(args):
         te = float(tt.item())
         e2e_timer = "host perf_counter, max over ranks: pinned H2D copy + reduce_multi + .item() per step"
     e2e = {"value": round(gbps(n * s * ws * ke, te), 3) if ke else None, "unit": "GB/s",
-           "h2d_bytes_per_step": n * s * ws, "d2h_bytes_per_step": s * ws,
+           "h2d_bytes_per_step": n * s * ws, "d2h_bytes_per_step": out.numel() * out.element_size() * ws,
            "steps": ke, "timer": e2e_timer}
 
     line = None
