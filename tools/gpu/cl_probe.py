@@ -1,3 +1,5 @@
+"""Small inputs: AUTO's plan vs the one-cluster kernel forced to 8 / 16 CTAs,
+graph-captured us per launch (the evidence for kClusterMaxBytes)."""
 import sys, os, json
 sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tools"))
 import torch
