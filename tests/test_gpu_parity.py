@@ -98,10 +98,29 @@ def test_bulk_variant_all_pairs(rd, dtype, op):
 
 
 def test_auto_planner_choice(rd):
+    """The AUTO plan: one CTA up to 32 KB, one cluster of <= 16 CTAs
+    up to 1 MiB, the vector grid (capped at 1 CTA/SM from 12 MiB, 2 from 48 MiB) below
+    128 MiB, the bulk ring from 128 MiB."""
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+
+    def plan(nbytes):
+        x = torch.zeros(nbytes // 4, dtype=torch.float32, device="cuda")
+        return rd.reduce_ex(x, "sum")[1]
+
+    p = plan(16 << 10)
+    assert p["variant"] == "vector" and p["grid"] == 1
+    p = plan(256 << 10)
+    assert p["variant"] == "cluster" and 2 <= p["grid"] <= 16
+    p = plan(1 << 20)
+    assert p["variant"] == "cluster" and p["grid"] == 16
+    assert plan(4 << 20)["variant"] == "vector"
+    p = plan(16 << 20)
+    assert p["variant"] == "vector" and p["grid"] == sms
+    p = plan(64 << 20)
+    assert p["variant"] == "vector" and p["grid"] == 2 * sms
+    assert plan(128 << 20)["variant"] == "bulk"
     small = to_dev(inputs.generate(1 << 20, "float32", "u01"))
-    big = torch.empty(1 << 25, dtype=torch.float32, device="cuda")
     assert rd.reduce_ex(small, "sum")[1]["variant"] == "vector"
-    assert rd.reduce_ex(big.zero_(), "sum")[1]["variant"] == "bulk"
 
 
 @pytest.mark.parametrize("dtype,op", [("float32", "sum"), ("int64", "prod"), ("float64", "max"),
