@@ -676,11 +676,12 @@ __device__ __forceinline__ void exact_finish_cluster(Ex (&ex)[E], uint32_t flags
     const unsigned G = cluster_nctarank();
     if (threadIdx.x <= NW) {
       const int j = threadIdx.x;
+      long long v[16];                               // all G remote loads in flight at once
+#pragma unroll
+      for (unsigned r = 0; r < 16; ++r) v[r] = r < G ? dsmem_load_i64(cta + j, r) : 0;
       long long s = 0;
-      for (unsigned r = 0; r < G; ++r) {
-        const long long v = dsmem_load_i64(cta + j, r);
-        s = (j == NW) ? (s | v) : (s + v);
-      }
+#pragma unroll
+      for (unsigned r = 0; r < 16; ++r) s = (j == NW) ? (s | v[r]) : (s + v[r]);
       if (j < NW) sacc[0][j] = s;
       else s_flags = (unsigned)s;
     }

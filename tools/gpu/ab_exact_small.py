@@ -1,0 +1,23 @@
+import ctypes, json, os, sys
+import torch
+L = ctypes.CDLL(sys.argv[1])
+L.reduce.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+out = torch.empty(2, dtype=torch.int64, device="cuda")
+res = {}
+for log2n in (14, 16, 18):
+    x = torch.rand(1 << log2n, device="cuda")
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        L.reduce(x.data_ptr(), x.numel(), 3, 10, out.data_ptr(), gs.cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=gs):
+        for _ in range(100):
+            L.reduce(x.data_ptr(), x.numel(), 3, 10, out.data_ptr(), gs.cuda_stream)
+    ts = []
+    for _ in range(7):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); g.replay(); b.record(); b.synchronize()
+        ts.append(a.elapsed_time(b) * 10.0)
+    res[f"2^{log2n}"] = round(sorted(ts)[3], 3)
+print(json.dumps({"lib": os.path.basename(sys.argv[1]), **res}))
