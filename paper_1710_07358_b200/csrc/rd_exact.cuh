@@ -137,6 +137,73 @@ __device__ __forceinline__ void sacc_normalise(long long* w) {
   w[NW - 1] += c;
 }
 
+// The same result as sacc_normalise, by one whole (converged) warp: lane l
+// owns words [l*R, l*R + R). Each lane carries its own words, then the lanes'
+// carries move one lane per shift step until they are all in {-1, 0, +1} and
+// of one sign, when a carry-lookahead over ballots (generate = the lane's
+// carry, propagate = its digits all ones for +1 / all zero for -1) settles
+// every ripple chain in one step -- the chain of 0xffffffff digits a negative
+// total leaves above its top digit included. The value is kept at every step,
+// and the digits of a value are unique, so the words equal the sequential's.
+template <int NW>
+__device__ __forceinline__ void sacc_normalise_warp(long long* w) {
+  constexpr int R = (NW + 31) / 32;
+  constexpr int L = (NW + R - 1) / R;                 // lanes that own words; L-1 owns the top word
+  constexpr long long M = 0xffffffffll;
+  const int ln = threadIdx.x & 31, k0 = ln * R;
+  const bool top = ln == L - 1;
+  long long d[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) d[i] = (ln < L && k0 + i < NW) ? w[k0 + i] : 0;
+  long long c = 0, hi = 0;                            // hi: the top lane's carry out (kept, not shipped)
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if (k0 + i < NW) { const long long t = d[i] + c; d[i] = t & M; c = t >> 32; }
+  if (top) { hi = c; c = 0; }
+  const unsigned below_top = (1u << (L - 1)) - 1u;    // lanes whose carry goes to the next lane
+  while (__any_sync(0xffffffffu, c != 0)) {
+    const unsigned gp = __ballot_sync(0xffffffffu, c == 1), gm = __ballot_sync(0xffffffffu, c == -1);
+    const bool lookahead = __all_sync(0xffffffffu, c >= -1 && c <= 1) && (gp == 0u || gm == 0u);
+    long long cin;
+    const bool gen = c != 0;
+    if (lookahead) {
+      const bool plus = gp != 0u;
+      bool prop = ln < L - 1;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+        if (k0 + i < NW) prop = prop && d[i] == (plus ? M : 0);
+      const unsigned G = plus ? gp : gm;
+      const unsigned P = __ballot_sync(0xffffffffu, prop) & below_top & ~G;
+      const unsigned into = ((G | P) + G) ^ P;        // bit l: a unit enters lane l
+      cin = ((into >> ln) & 1u) ? (plus ? 1 : -1) : 0;
+    } else {
+      cin = __shfl_up_sync(0xffffffffu, c, 1);
+      if (ln == 0) cin = 0;
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (k0 + i < NW) { const long long t = d[i] + cin; d[i] = t & M; cin = t >> 32; }
+    // cin is now the lane's carry out: the top lane keeps it; after a shift
+    // step it is the lane's next carry; after a lookahead step the chains
+    // already account for a propagating lane's, and only a generating lane
+    // that also wrapped has one left
+    if (top) { hi += cin; c = 0; }
+    else c = (!lookahead || gen) ? cin : 0;
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+    if (ln < L && k0 + i < NW) w[k0 + i] = d[i] + ((k0 + i == NW - 1) ? (long long)((unsigned long long)hi << 32) : 0);
+}
+
+// what a whole warp calls: the lookahead form for the fp64 68 words (measured
+// ~0.45 us less per small launch), lane 0's sequential carry for fp32's 12
+// (there the warp form costs ~0.1 us more; profiles/r01_exact_small_norm.txt)
+template <int NW>
+__device__ __forceinline__ void sacc_normalise_by_warp(long long* w) {
+  if constexpr (NW > 32) sacc_normalise_warp<NW>(w);
+  else if ((threadIdx.x & 31) == 0) sacc_normalise<NW>(w);
+}
+
 // ------------------------------------------------------------------ expansions
 struct Ex { double a0, a1, a2; };   // a0 + a1 + a2 exactly; |a0| >> |a1| >> |a2| in practice
 
@@ -563,7 +630,7 @@ __device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], uint32_t flags, lon
   if (ln == 0 && flags) atomicOr(&s_flags, flags);
   __syncwarp();
   // a4: each warp carries its words into digits
-  if (ln == 0) sacc_normalise<NW>(w);
+  sacc_normalise_by_warp<NW>(w);
   __syncthreads();
   // a5: the CTA's words (sum of NWARP digit vectors)
   if (threadIdx.x < NW) {
@@ -645,8 +712,8 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
     else s_flags = (unsigned)s;
   }
   __syncthreads();
+  if (threadIdx.x < 32) sacc_normalise_by_warp<NW>(sacc[0]);
   if (threadIdx.x == 0) {
-    sacc_normalise<NW>(sacc[0]);
     *args.ticket = 0u;
     if (args.work) *args.work = 0u;
   }
@@ -686,7 +753,7 @@ __device__ __forceinline__ void exact_finish_cluster(Ex (&ex)[E], uint32_t flags
       else s_flags = (unsigned)s;
     }
     __syncthreads();
-    if (threadIdx.x == 0) sacc_normalise<NW>(sacc[0]);
+    if (threadIdx.x < 32) sacc_normalise_by_warp<NW>(sacc[0]);
     __syncthreads();
     exact_emit<T>(sacc[0], s_flags, args);
   }

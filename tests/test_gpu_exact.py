@@ -237,3 +237,36 @@ def test_exact_cluster_small_sizes(rd, dtype):
         torch.cuda.synchronize()
         for c in comms:
             c.destroy()
+
+
+@pytest.mark.parametrize("dtype", FLT)
+def test_exact_carry_chains(rd, dtype):
+    """Totals whose carried words are long ripple chains (the warp carry-lookahead
+    in rd_exact.cuh sacc_normalise_warp): a tiny negative total leaves a run of
+    0xffffffff digits up to the top word; a huge value cancelled by its negative
+    up to one subnormal crosses every word; both signs at once in one launch."""
+    fi = np.finfo(dtype)
+    tiny = fi.smallest_subnormal
+    rng = np.random.default_rng(5)
+    cases = []
+    for n in (1, 33, 4099, (1 << 16) + 7, (1 << 20) + 3):
+        for sgn in (-1.0, 1.0):
+            x = np.zeros(n, dtype)
+            x[n // 2] = sgn * tiny                                     # one subnormal unit
+            cases.append(x)
+            y = rng.standard_normal(n).astype(dtype) * np.asarray(2.0, dtype) ** rng.integers(-40, 40, n).astype(dtype)
+            y = np.concatenate([y[:n // 2], [sgn * tiny], -y[::-1], y[n // 2:]]).astype(dtype)  # cancels up to +-tiny
+            cases.append(y)
+            z = np.zeros(n, dtype)
+            z[0], z[-1] = fi.max, -fi.max
+            if n > 2:
+                z[1] = sgn * tiny
+            cases.append(z)
+    for x in cases:
+        want = oracle.reduce(x, "sum_exact").value
+        xd = to_dev(x, 1)
+        for variant in ("auto", "vector", "bulk", "cluster"):
+            got = rd.reduce_ex(xd, "sum_exact", variant=variant)[0]
+            assert same(val(got), want), (dtype, len(x), variant)
+        rec = rd.reduce_exact_partial(xd)
+        assert same(val(rd.combine_exact_records(rec, dtype)), want)
