@@ -523,6 +523,11 @@ __device__ __noinline__ void exact_fused_exchange(long long* words, unsigned fla
     }
   }
   __syncwarp();
+  // timeout, bad and n are warp-uniform (every lane read the same headers)
+  if (!timeout && !bad && n != 0) {
+    sacc_normalise_by_warp<NW>(words);
+    __syncwarp();
+  }
   if (ln == 0) {
     if (timeout) atomicExch(args.err, (int)RD_ERR_TIMEOUT);
     else if (bad) atomicExch(args.err, (int)RD_ERR_MISMATCH);
@@ -530,7 +535,6 @@ __device__ __noinline__ void exact_fused_exchange(long long* words, unsigned fla
       if constexpr (sizeof(T) == 4) *(uint32_t*)args.out = 0u;
       else *(uint64_t*)args.out = 0ull;
     } else {
-      sacc_normalise<NW>(words);
       exact_store<T>(words, fl, n, args.out);
     }
     *(volatile unsigned long long*)&args.self->epoch = epoch;
@@ -995,8 +999,10 @@ __global__ void rd_exact_combine_kernel(const rd_exact_record* recs, int count, 
     s[threadIdx.x] = a;
   }
   __syncthreads();
+  if (threadIdx.x >= 32) return;
+  sacc_normalise_by_warp<NW>(s);                    // launched with 128 threads: warp 0 is whole
+  __syncwarp();
   if (threadIdx.x != 0) return;
-  sacc_normalise<NW>(s);
   if (s_bad && d_status) *d_status = (int)RD_ERR_MISMATCH;
   if (out) {
     if (s_bad || s_n == 0) {
