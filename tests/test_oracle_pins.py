@@ -113,15 +113,20 @@ def test_absorption_golden():
     # the paper's claim, pinned with the independent brute-force enumerator
     for prec in FLOAT_DTYPES:
         assert _brute.tree_results([1.5, big, -big], "sum", prec) == {0.0, 1.5}
-    # fp32 oracle: fp64 accumulator absorbs 1.5 in the left fold (2^100 ulp is 2^48)
+    # the golden left fold in each precision (the plain fold the footnote describes)
     for order, want in [([1.5, big, -big], 0.0), ([big, -big, 1.5], 1.5)]:
-        x = np.array(order, dtype=np.float32)
-        assert float(oracle.reduce(x, "sum").value) == want
-    # fp64 oracle: double-double accumulator keeps 1.5 in both orders (the exact sum)
-    for order in ([1.5, big, -big], [big, -big, 1.5], [big, 1.5, -big]):
-        r = oracle.reduce(np.array(order, dtype=np.float64), "sum")
-        assert float(r.value) == 1.5
-        assert r.sum_abs == 2 * big + 1.5
+        for prec in FLOAT_DTYPES:
+            acc = np.array([order[0]], dtype=prec)[0]
+            for t in order[1:]:
+                acc = acc + np.array([t], dtype=prec)[0]
+            assert float(acc) == want
+    # the oracle: its double-double accumulator (fp32 and fp64 data) keeps 1.5 in every
+    # order -- the exact sum the footnote calls "always the same"
+    for prec in FLOAT_DTYPES:
+        for order in ([1.5, big, -big], [big, -big, 1.5], [big, 1.5, -big]):
+            r = oracle.reduce(np.array(order, dtype=prec), "sum")
+            assert float(r.value) == 1.5
+            assert r.sum_abs == 2 * big + 1.5
 
 
 def test_compensation_golden():
@@ -177,16 +182,18 @@ def test_float_sum_brute_force_contains_exact(prec):
 @pytest.mark.parametrize("prec", FLOAT_DTYPES)
 @pytest.mark.parametrize("wl", ["u01", "normalish"])
 def test_float_sum_exact_referee(prec, wl):
-    """|oracle - exact| within the oracle's own rounding (fp64: plain fold bound
-    (n-1)*2^-53*sum|x|; double-double: 4n*2^-104*sum|x|) + 1/2 ulp of the final rounding."""
+    """|oracle - exact| within the oracle's own rounding (double-double, fp32 and fp64
+    data: 4n*2^-104*sum|x|) + 1/2 ulp of the final rounding (+ the fp64 step of fp32 data)."""
     for n in [1, 2, 3, 17, 1000, 4099]:
         x = inputs.generate(n, prec, wl, seed=n)
         r = oracle.reduce(x, "sum")
         ex = _brute.exact_sum(x)
         sabs = float(sum(abs(_brute.Fraction(float(t))) for t in x))
-        acc_err = (n - 1) * 2.0 ** -53 * sabs if prec == "float32" else 4 * n * 2.0 ** -104 * sabs
-        assert abs(r.exact - float(ex)) <= acc_err + 1e-300
-        assert abs(float(r.value) - float(ex)) <= 0.5 * _brute.ulp(float(r.value), prec) + acc_err
+        acc_err = 4 * n * 2.0 ** -104 * sabs
+        got = _brute.Fraction(r.hi) + _brute.Fraction(r.lo)     # the unrounded double-double
+        assert abs(got - ex) <= _brute.Fraction(acc_err)
+        step = 2.0 ** -53 * abs(float(ex)) if prec == "float32" else 0.0   # hi + lo -> fp64 -> fp32
+        assert abs(float(r.value) - float(ex)) <= 0.5 * _brute.ulp(float(r.value), prec) + acc_err + step
         assert math.isclose(r.sum_abs, sabs, rel_tol=1e-15)
 
 
@@ -196,9 +203,11 @@ def test_float_prod_exact_referee(prec):
         x = inputs.generate(n, prec, "near_one", seed=n + 11)
         r = oracle.reduce(x, "prod")
         ex = float(_brute.exact_prod(x))
-        acc_err = (n - 1) * 2.0 ** -53 * abs(ex) if prec == "float32" else 4 * n * 2.0 ** -104 * abs(ex)
-        assert abs(r.exact - ex) <= acc_err * 1.0000001 + 1e-300
-        assert abs(float(r.value) - ex) <= 0.5 * _brute.ulp(float(r.value), prec) + acc_err * 1.0000001
+        acc_err = 4 * n * 2.0 ** -104 * abs(ex)
+        got = _brute.Fraction(r.hi) + _brute.Fraction(r.lo)
+        assert abs(got - _brute.exact_prod(x)) <= _brute.Fraction(acc_err * 1.0000001)
+        step = 2.0 ** -53 * abs(ex) if prec == "float32" else 0.0
+        assert abs(float(r.value) - ex) <= 0.5 * _brute.ulp(float(r.value), prec) + acc_err * 1.0000001 + step
 
 
 def test_plain_fp64_fold_is_not_enough():
@@ -214,6 +223,52 @@ def test_plain_fp64_fold_is_not_enough():
     err_oracle = abs(_brute.Fraction(float(oracle.reduce(x, "sum").value)) - ex)
     assert err_oracle <= _brute.Fraction(math.ulp(float(ex))) / 2
     assert err_plain > 4 * err_oracle
+
+
+def test_fp32_data_plain_fp64_fold_is_not_enough():
+    """Why fp32 data also take the double-double accumulator (a plain fp64 fold
+    of fp32 data can err by (n-1) 2^-53 sum|x| = 16 eps32 sum|x| at n = 2^34, above the 4 eps32
+    tolerance it referees): 2^30 followed by 2^-30 terms -- each is absorbed by a plain fp64
+    running sum (2^30 + 2^-30 needs 61 bits), the double-double keeps every one exactly."""
+    k = 3000
+    x = np.array([2.0 ** 30] + [2.0 ** -30] * k, dtype=np.float32)
+    ex = _brute.exact_sum(x)
+    plain = 0.0
+    for t in x.tolist():
+        plain += t
+    assert plain == 2.0 ** 30 and _brute.Fraction(plain) != ex
+    r = oracle.reduce(x, "sum")
+    assert _brute.Fraction(r.hi) + _brute.Fraction(r.lo) == ex
+    r = oracle.reduce(x[::-1].copy(), "sum")            # small terms first: exact either way
+    assert _brute.Fraction(r.hi) + _brute.Fraction(r.lo) == ex
+
+
+@pytest.mark.parametrize("prec", FLOAT_DTYPES)
+@pytest.mark.parametrize("op,wl", [("sum", "u01"), ("sum", "normalish"), ("sum", "wide"), ("prod", "near_one")])
+def test_merge_float_branch_vs_fraction(prec, op, wl):
+    """or_merge's float + / x branch (the rank-order combine of the host-logic tests) against
+    exact rationals on split arrays, at the double-double bound 4n 2^-104 sum|x| (+) /
+    8n 2^-104 |prod| (x): a dropped lo word (the merge adding only hi) misses it by ~2^-53."""
+    n = 3001
+    x = inputs.generate(n, prec, wl, seed=21)
+    if op == "sum":
+        ex = _brute.exact_sum(x)
+        bound = _brute.Fraction(4 * n * 2.0 ** -104) * sum(abs(_brute.Fraction(float(t))) for t in x)
+    else:
+        ex = _brute.exact_prod(x)
+        bound = _brute.Fraction(8 * n * 2.0 ** -104) * abs(ex)
+    for cuts in ([1], [1500], [2999], [7, 700, 2000, 3000]):
+        parts = np.split(x, cuts)
+        acc = oracle.Fold(prec, op)
+        for p in parts:
+            acc.merge(oracle.Fold(prec, op).fold(p))
+        r = acc.result()
+        assert r.count == n
+        got = _brute.Fraction(r.hi) + _brute.Fraction(r.lo)
+        assert abs(got - ex) <= bound, (cuts, float(got - ex))
+        # and the merged fold is the one-shot fold's value
+        one = oracle.reduce(x, op)
+        assert abs(float(r.value) - float(one.value)) <= _brute.ulp(float(one.value), prec)
 
 
 # ------------------------------------------------------ exact-representable workloads
