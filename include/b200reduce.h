@@ -36,9 +36,15 @@
  *    unsigned for uint32; AND/OR/XOR on raw bits. Bit-exact for any order.
  *  - float min/max: IEEE 754-2019 minimum/maximum (NaN propagates as a quiet
  *    NaN, -0.0 < +0.0). Bit-exact.
- *  - float +: fp32 accumulates in fp32, fp64 in fp64, in a fixed tree order;
- *    |result - exact| <= 4 * eps(dtype) * sum|x_i| on the workloads of
- *    DESIGN.md. A zero sum is -0.0 iff every x_i is -0.0; empty -> +0.0.
+ *  - float +: blocked pairwise summation in a fixed order -- each thread sums
+ *    the <= 32 elements it loads per iteration as a balanced tree in the
+ *    input precision and adds the block sums into a wide accumulator (fp64
+ *    for fp32 data, double-double for fp64 data), in which every later
+ *    combine happens; one rounding at the end. For EVERY input whose partial
+ *    sums stay finite (e.g. sum|x_i| <= the dtype's largest finite value):
+ *    |result - exact| <= 3.01 * eps(dtype) * sum|x_i|, inside the north-star
+ *    bound 4 * eps * sum|x_i| (R6). A zero sum is -0.0 iff every
+ *    x_i is -0.0; empty -> +0.0.
  *  - float x: fp32 accumulates in fp64, fp64 in double-double, then one
  *    rounding; |result - exact| <= 4 * eps(dtype) * |exact| when no partial
  *    product over/underflows.
@@ -75,8 +81,9 @@ typedef enum {
    * ... Kahan"): fp32 accumulates in fp64, fp64 in double-double (TwoSum per
    * term), so the result is the exact sum rounded once except in near-tie
    * cases -- in practice independent of order, grid and GPU count.
-   * |result - exact| <= 0.5 ulp(result) + 4 * u_acc * sum|x_i| on the
-   * workloads of DESIGN.md, u_acc = 2^-53 (fp32 data) / 2^-106 (fp64 data).
+   * |result - exact| <= 0.5 ulp(result) + d * u_acc * sum|x_i| for every
+   * input with finite partial sums, d < 2^21 the depth of the kernels' wide
+   * chains (R16), u_acc = 2^-53 (fp32 data) / ~2^-104 (fp64 data).
    * Integers: identical to RD_SUM. */
   RD_SUM_COMPENSATED = 9,
   /* SURVEY §8(f) f2, reproducible: the EXACT sum rounded once (round to
@@ -122,8 +129,8 @@ typedef struct CUstream_st* rd_stream_t;
  *   tag    = 0x52440000 | dtype << 8 | op      (0 marks "no record")
  *   status = 0 (reserved)
  *   n      = number of elements the partial covers
- *   acc    = the accumulator bits (integer value; fp32 +: float bits;
- *            fp32 x / fp64 +: double bits; fp64 x: double-double hi, lo;
+ *   acc    = the accumulator bits (integer value; fp32 + and x: double
+ *            bits; fp64 + and x: double-double hi, lo;
  *            float min/max: order-preserving key and the max |x| bit pattern;
  *            argmin/argmax: order key and the index WITHIN the block, which
  *            rd_combine_records shifts by the n of the records before it)

@@ -9,8 +9,10 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# RD_LIB_PATH: load another build of the same ABI (A/B measurements only)
-LIB_PATH = os.environ.get("RD_LIB_PATH") or os.path.join(_HERE, "libb200reduce.so")
+# the in-tree build, always (no environment override: the product path loads
+# exactly this library; measurement tools that A/B other builds load those
+# .so files themselves, tools/ab_lib.py)
+LIB_PATH = os.path.join(_HERE, "libb200reduce.so")
 
 RD_INT32, RD_UINT32, RD_INT64, RD_FLOAT32, RD_FLOAT64 = range(5)
 RD_SUM, RD_PROD, RD_MIN, RD_MAX, RD_AND, RD_OR, RD_XOR = range(7)

@@ -1,8 +1,12 @@
 """Build the in-tree native libraries for sm_100a.
 
-    python -m paper_1710_07358_b200.build [--force]
+    python -m paper_1710_07358_b200.build [--force] [--tuning]
 
 - paper_1710_07358_b200/libb200reduce.so   the product (C ABI: include/b200reduce.h)
+- build/tuning/libb200reduce.so             --tuning only: the same ABI compiled with
+                                            -DRD_TUNING (reads the RD_TUNE_* knobs and
+                                            carries the alternative exact-sum shapes;
+                                            measurement tools load it explicitly)
 - inputs/libinputs_host.so, inputs/libinputs_device.so   seeded generators
 - oracle/liboracle.so                       the CPU checker (test infrastructure;
                                             building it is not using it)
@@ -23,6 +27,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libb200reduce.so")
+TUNING_OBJ = os.path.join(ROOT, "build", "obj_tuning")
+TUNING_LIB = os.path.join(ROOT, "build", "tuning", "libb200reduce.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -43,10 +49,11 @@ def _stale(out, srcs):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def _compile(src: str, force: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+def _compile(src: str, force: bool, tuning: bool = False) -> str:
+    obj = os.path.join(TUNING_OBJ if tuning else OBJ, os.path.basename(src).replace(".cu", ".o"))
     if force or _stale(obj, [src] + _deps()):
         cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+               *(["-DRD_TUNING"] if tuning else []),
                "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(nccl_dir(), "include"),
                "-c", src, "-o", obj + ".tmp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -58,19 +65,21 @@ def _compile(src: str, force: bool) -> str:
     return obj
 
 
-def build_library(force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build_library(force: bool = False, tuning: bool = False) -> str:
+    lib = TUNING_LIB if tuning else LIB
+    os.makedirs(TUNING_OBJ if tuning else OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=max(2, os.cpu_count() or 2)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force), srcs))
-    if force or _stale(LIB, objs):
+        objs = list(ex.map(lambda s: _compile(s, force, tuning), srcs))
+    if force or _stale(lib, objs):
         nd = nccl_dir()
-        cmd = ["nvcc", *ARCH, "-shared", "-o", LIB + ".tmp", *objs,
+        cmd = ["nvcc", *ARCH, "-shared", "-o", lib + ".tmp", *objs,
                "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
                "-Xlinker", f"-rpath={os.path.join(nd, 'lib')}"]
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(lib + ".tmp", lib)
+    return lib
 
 
 def build_probe(force: bool = False) -> str:
@@ -96,5 +105,8 @@ def build_all(force: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    build_all(force="--force" in sys.argv)
-    print(LIB)
+    if "--tuning" in sys.argv:
+        print(build_library(force="--force" in sys.argv, tuning=True))
+    else:
+        build_all(force="--force" in sys.argv)
+        print(LIB)

@@ -145,11 +145,11 @@ bool lookup(int dtype, int op, int variant, int unroll, int vec_bytes, KernelRef
   return lookup_int(dtype, op, variant, unroll, vec_bytes, r);
 }
 
-// Tuning knobs for the bulk chunk schedule (measurement only; the defaults
-// are the documented schedule). They are constants of the schedule, so the
-// result stays a function of n and the alignment for a fixed environment.
+// Tuning knobs for the bulk chunk schedule and the mid-size grid cap: read
+// only by RD_TUNING builds (rd_internal.h tune_env); the shipped library
+// always takes the defaults, the documented schedule.
 uint64_t env_u64(const char* name, uint64_t dflt) {
-  const char* v = std::getenv(name);
+  const char* v = tune_env(name);
   if (!v || !*v) return dflt;
   const unsigned long long x = std::strtoull(v, nullptr, 10);
   return x ? (uint64_t)x : dflt;
@@ -343,8 +343,8 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     // from 12 MiB, 1 CTA/SM up to 48 MiB and 2 above (tools/sweep.py midops,
     // graph-captured, 7 (dtype, op): 7-16% faster at 16-64 MB; below 12 MiB
     // the cap cost up to 12%, so it does not apply there).
-    // RD_TUNE_VEC_CTAS_PER_SM (measurement only): 0 / unset = this rule, k = k CTAs
-    // per SM from 12 MiB, kNoCap = the uncapped occupancy grid.
+    // RD_TUNE_VEC_CTAS_PER_SM (RD_TUNING builds only): 0 / unset = this rule,
+    // k = k CTAs per SM from 12 MiB, kNoCap = the uncapped occupancy grid.
     constexpr uint64_t kNoCap = 1000;
     static const uint64_t kMidCap = env_u64("RD_TUNE_VEC_CTAS_PER_SM", 0);
     if (k.variant == RD_VARIANT_VECTOR && kMidCap != kNoCap && (uint64_t)n * s >= (12ull << 20)) {
@@ -445,7 +445,7 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
                  !(cfg && cfg->grid > kClusterMax)) ? RD_VARIANT_CLUSTER : RD_VARIANT_VECTOR;
   }
   ExactRef k;
-  if (!lookup_exact(dtype, variant, &k)) { set_error("no compiled exact-sum kernel (RD_TUNE_EXACT?)"); return RD_ERR_UNSUPPORTED; }
+  if (!lookup_exact(dtype, variant, &k)) { set_error("no compiled exact-sum kernel"); return RD_ERR_UNSUPPORTED; }
   if (cfg && ((cfg->unroll && cfg->unroll != k.unroll) || (cfg->vec_bytes && cfg->vec_bytes != k.vec_bytes) ||
               (cfg->block && cfg->block != k.block))) {
     set_error("RD_SUM_EXACT: one compiled configuration per variant (vector: 32 B loads, U=6, 256 threads; "

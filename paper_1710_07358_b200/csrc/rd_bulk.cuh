@@ -183,14 +183,28 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
         uint4 v[PER_THREAD];
 #pragma unroll
         for (int k = 0; k < PER_THREAD; ++k) v[k] = lds128(base + (k * CT + t) * 16);
+        T xs[PER_THREAD][L];
 #pragma unroll
         for (int k = 0; k < PER_THREAD; ++k) {
           Vec<16> w{{v[k].x, v[k].y, v[k].z, v[k].w}};
-          T xs[L];
 #pragma unroll
-          for (int l = 0; l < L; ++l) xs[l] = lane<T, 16>(w, l);
-          LO::fold_vec(acc, xs, step0 + k);
+          for (int l = 0; l < L; ++l) xs[k][l] = lane<T, 16>(w, l);
         }
+        LO::fold_vecs(acc, xs, step0);
+      } else if constexpr (Blocked<OpT>::value) {
+        // a short stage (the chunk's last): missing vectors are the identity
+        // -0.0, so the block tree is the same as for a full stage
+        T xs[PER_THREAD][L];
+#pragma unroll
+        for (int k = 0; k < PER_THREAD; ++k) {
+          const uint32_t off = (k * CT + t) * 16;
+          uint4 q = make_uint4(0, 0, 0, 0);
+          if (off < bytes) q = lds128(base + off);
+          Vec<16> w{{q.x, q.y, q.z, q.w}};
+#pragma unroll
+          for (int l = 0; l < L; ++l) xs[k][l] = off < bytes ? lane<T, 16>(w, l) : (T)(-0.0);
+        }
+        LO::fold_vecs(acc, xs, step0);
       } else {
 #pragma unroll
         for (int k = 0; k < PER_THREAD; ++k) {

@@ -4,13 +4,14 @@
 #include <cstdlib>
 
 #include "rd_exact.cuh"
+#include "rd_internal.h"
 #include "rd_registry.h"
 
 namespace rd {
 
-// Tuning only (measurement): RD_TUNE_EXACT="U,E,M" picks another compiled
-// (loads in flight, expansions, min CTAs/SM for the register cap); the
-// default is the measured best.
+// RD_TUNING builds only: RD_TUNE_EXACT="U,E,M" picks another compiled
+// configuration (loads in flight, expansions, min CTAs/SM for the register
+// cap); the default is the measured best and the only one shipped.
 template <typename T>
 static bool pick(int u, int e, int m, ExactRef* r) {
 #define RD_X(U, E, M)                                                                              \
@@ -18,7 +19,10 @@ static bool pick(int u, int e, int m, ExactRef* r) {
     *r = ExactRef{rd_exact_kernel<T, kBlock, U, E, M>, kBlock, U, 32};                            \
     return true;                                                                                   \
   }
-  RD_X(6, 2, 2) RD_X(6, 2, 1) RD_X(4, 2, 2) RD_X(8, 1, 2) RD_X(2, 2, 3)
+  RD_X(6, 2, 2)
+#ifdef RD_TUNING
+  RD_X(6, 2, 1) RD_X(4, 2, 2) RD_X(8, 1, 2) RD_X(2, 2, 3)
+#endif
 #undef RD_X
   return false;
 }
@@ -30,22 +34,24 @@ static bool bulk_ref(ExactRef* r) {
   return true;
 }
 
-// Tuning only: RD_TUNE_EXACT_BULK="CW,E" (consumer warps, expansions)
+// RD_TUNING builds only: RD_TUNE_EXACT_BULK="CW,E" (consumer warps, expansions)
 template <typename T>
 static bool pick_bulk(ExactRef* r) {
   static int tcw = 0, te = 0;
   static bool once = [] {
-    const char* v = std::getenv("RD_TUNE_EXACT_BULK");
+    const char* v = tune_env("RD_TUNE_EXACT_BULK");
     if (v && std::sscanf(v, "%d,%d", &tcw, &te) != 2) tcw = te = 0;
     return true;
   }();
   (void)once;
   const int cw = tcw ? tcw : kExactBulkConsumerWarps, e = te ? te : kExactBulkExpansions;
-  if (cw == 16 && e == 2) return bulk_ref<T, 16, 2>(r);
   if (cw == 16 && e == 1) return bulk_ref<T, 16, 1>(r);
+#ifdef RD_TUNING
+  if (cw == 16 && e == 2) return bulk_ref<T, 16, 2>(r);
   if (cw == 24 && e == 1) return bulk_ref<T, 24, 1, 5, 24576>(r);
   if (cw == 24 && e == 2) return bulk_ref<T, 24, 2, 5, 24576>(r);
   if (cw == 8 && e == 2) return bulk_ref<T, 8, 2>(r);
+#endif
   return false;
 }
 
@@ -70,7 +76,7 @@ bool lookup_exact(int dtype, int variant, ExactRef* r) {
   }
   static int tu = 0, te = 0, tm = 0;
   static bool once = [] {
-    const char* v = std::getenv("RD_TUNE_EXACT");
+    const char* v = tune_env("RD_TUNE_EXACT");
     if (v && std::sscanf(v, "%d,%d,%d", &tu, &te, &tm) != 3) tu = te = tm = 0;
     return true;
   }();

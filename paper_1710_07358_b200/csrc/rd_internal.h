@@ -3,11 +3,22 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "b200reduce.h"
 
 namespace rd {
+
+// Tuning knobs are for measurement builds only (`python -m
+// paper_1710_07358_b200.build --tuning` defines RD_TUNING and writes
+// build/tuning/libb200reduce.so). The shipped library reads no environment
+// variable: its results are a function of the call's arguments alone.
+#ifdef RD_TUNING
+inline const char* tune_env(const char* name) { return std::getenv(name); }
+#else
+inline const char* tune_env(const char*) { return nullptr; }
+#endif
 
 // thread-local detail for rd_last_error()
 void set_error(const std::string& msg);

@@ -377,21 +377,20 @@ __device__ __forceinline__ typename OpT::Acc vector_body(const KArgs& args, type
       Vec<VB> v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
+      T xs[U][L];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        T xs[L];
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int l = 0; l < L; ++l) xs[l] = lane<T, VB>(v[u], l);
-        LO::fold_vec(acc, xs, step + u);
-      }
+        for (int l = 0; l < L; ++l) xs[u][l] = lane<T, VB>(v[u], l);
+      LO::fold_vecs(acc, xs, step);
     }
   }
   for (; i < nvec; i += stride, ++step) {
     Vec<VB> v = ldg_stream<VB>(body + i * VB);
-    T xs[L];
+    T xs[1][L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) xs[l] = lane<T, VB>(v, l);
-    LO::fold_vec(acc, xs, step);
+    for (int l = 0; l < L; ++l) xs[0][l] = lane<T, VB>(v, l);
+    LO::fold_vecs(acc, xs, step);
   }
   pdl_trigger();
   // a3: lanes -> one accumulator (indexed ops: element index = head + (tid + step*stride)*L + lane)
@@ -463,9 +462,15 @@ __global__ void __launch_bounds__(B) rd_paper_kernel(const KArgs args) {
     T v[F];
 #pragma unroll
     for (int k = 0; k < F; ++k) v[k] = (pos + k < n) ? __ldg(x + pos + k) : T{};
+    if constexpr (Blocked<OpT>::value) {   // the F elements as one tree (FloatSum)
 #pragma unroll
-    for (int k = 0; k < F; ++k)
-      if (pos + k < n) acc = fold_at<OpT>(acc, v[k], pos + k);
+      for (int k = 0; k < F; ++k) v[k] = (pos + k < n) ? v[k] : (T)(-0.0);
+      add_blocks<OpT, F>(acc, v);
+    } else {
+#pragma unroll
+      for (int k = 0; k < F; ++k)
+        if (pos + k < n) acc = fold_at<OpT>(acc, v[k], pos + k);
+    }
   }
   acc = block_reduce<OpT, B>(acc, smem);
   __syncthreads();

@@ -97,36 +97,6 @@ struct IntOp {
   __device__ __forceinline__ static Acc unpack(Slot s) { return (Acc)s.a; }
 };
 
-// ------------------------------------------------------------ float32 / float64 +
-template <typename F>
-struct FloatSum {
-  using T = F;
-  using Acc = F;
-  static constexpr bool kFloat = true;
-  static constexpr bool kIndexed = false;
-  __device__ __forceinline__ static Acc identity() { return (F)(-0.0); }
-  __device__ __forceinline__ static Acc combine(Acc a, Acc b) { return a + b; }
-  __device__ __forceinline__ static Acc fold(Acc a, T x) { return a + x; }
-  __device__ __forceinline__ static Acc warp_reduce(Acc a) {
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-      if constexpr (sizeof(F) == 4) a = a + __shfl_xor_sync(0xffffffffu, a, m);
-      else a = a + shfl_xor_f64(a, m);
-    }
-    return a;
-  }
-  __device__ __forceinline__ static void store(Acc a, void* out) { *(T*)out = a; }
-  __device__ __forceinline__ static void store_empty(void* out) { *(T*)out = (F)0.0; }
-  __device__ __forceinline__ static Slot pack(Acc a) {
-    if constexpr (sizeof(F) == 4) return Slot{(uint64_t)__float_as_uint(a), 0};
-    else return Slot{(uint64_t)__double_as_longlong(a), 0};
-  }
-  __device__ __forceinline__ static Acc unpack(Slot s) {
-    if constexpr (sizeof(F) == 4) return __uint_as_float((uint32_t)s.a);
-    else return __longlong_as_double((long long)s.a);
-  }
-};
-
 // ------------------------------------------------- float32 x (fp64 accumulator)
 struct Float32Prod {
   using T = float;
@@ -332,6 +302,67 @@ struct Float64SumComp {
   }
 };
 
+// ------------------------------------------------ float32 / float64 + (RD_SUM)
+// The north-star bound |result - exact| <= 4 eps sum|x_i| for EVERY input
+// (whose partial sums stay finite: e.g. sum|x_i| <= the dtype's max) by
+// blocked pairwise summation, at the plain sum's cost per element:
+//   * the K <= 32 elements a thread has loaded in one iteration (U vectors in
+//     the vector kernel, one ring stage's slice in the bulk kernel) are summed
+//     as a balanced binary tree in the INPUT precision (depth t <= 5):
+//     |tree - sum| <= t u sum|x| (u = eps/2 = 2^-24 / 2^-53);
+//   * the block sum enters a WIDE accumulator exactly or nearly so: fp32 data
+//     -> fp64 (exact widening + one DADD), fp64 data -> double-double (TwoSum);
+//     every later combine (lanes, warp, CTA, chunk slots, records) stays wide,
+//     so chains of any length d add only d u_w sum|x| (u_w = 2^-53 / ~2^-106);
+//   * one rounding to the dtype at the end: <= u |S|.
+// Total <= (t + 1) u sum|x| + d u_w sum|x| < 3.01 eps sum|x|: t <= 5, and the
+// wide chains of these kernels are d < 2^21 deep for any n < 2^40 (DESIGN.md
+// R6) -- whatever the values, so no input can push a long input-precision
+// chain past the bound (per-lane fp32 chains missed it by 7x at 2^28 on an
+// input that places 1.0 at the head of every chain).
+// P:50 fn 3: "double precision floating points" as the mitigation, applied
+// to the block sums instead of to every element.
+template <typename F>
+struct FloatSum;
+
+template <>
+struct FloatSum<float> : Float32SumComp {
+  static constexpr bool kBlocked = true;
+  __device__ __forceinline__ static Acc add_block(Acc a, float s) { return __dadd_rn(a, (double)s); }
+};
+
+template <>
+struct FloatSum<double> : Float64SumComp {
+  static constexpr bool kBlocked = true;
+  __device__ __forceinline__ static Acc add_block(Acc a, double s) { return two_sum_into(a.hi, a.lo, s); }
+};
+
+template <class O, class = void> struct Blocked : std::false_type {};
+template <class O> struct Blocked<O, std::void_t<decltype(O::kBlocked)>> : std::bool_constant<O::kBlocked> {};
+
+// the largest block summed as one tree (depth <= 5)
+constexpr int kMaxTreeBlock = 32;
+
+// balanced binary tree over v[0..N) in the element precision: depth ceil(log2 N)
+template <int N, typename T>
+__device__ __forceinline__ T tree_sum(const T* v) {
+  if constexpr (N == 1) return v[0];
+  else {
+    constexpr int H = N / 2;
+    return tree_sum<N - H>(v) + tree_sum<H>(v + (N - H));
+  }
+}
+
+// acc <- acc (+) tree(v[C..C+32)) (+) tree(v[C+32..)) ... for a blocked sum
+template <class OpT, int N, int C = 0, typename T>
+__device__ __forceinline__ void add_blocks(typename OpT::Acc& acc, const T* v) {
+  if constexpr (C < N) {
+    constexpr int M = (N - C < kMaxTreeBlock) ? N - C : kMaxTreeBlock;
+    acc = OpT::add_block(acc, tree_sum<M>(v + C));
+    add_blocks<OpT, N, C + M>(acc, v);
+  }
+}
+
 // ------------------------------------------------- argmin / argmax
 // Value and the SMALLEST index attaining it (reading R6). Every element maps
 // to an unsigned order key K (ints: sign-flipped bits; floats: the total-order
@@ -506,6 +537,18 @@ struct LaneOps {
       for (int l = 0; l < L; ++l) acc[l] = OpT::fold(acc[l], x[l]);
     }
   }
+  // the K vectors one thread loaded in one iteration (vector k's elements
+  // come at step step0 + k). Blocked sums (FloatSum): one input-precision
+  // tree per <= 32 elements into the wide lane accumulator 0.
+  template <int K, int L>
+  __device__ __forceinline__ static void fold_vecs(Lane (&acc)[L], const T (&x)[K][L], uint32_t step0) {
+    if constexpr (Blocked<OpT>::value) {
+      add_blocks<OpT, K * L>(acc[0], &x[0][0]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) fold_vec(acc, x[k], step0 + k);
+    }
+  }
   template <int L, class F>
   __device__ __forceinline__ static typename OpT::Acc finish(const Lane (&acc)[L], F) {
     typename OpT::Acc a = acc[0];
@@ -555,6 +598,11 @@ struct LaneOps<OpT, true> {
         acc[l] = better ? Lane{k, step} : acc[l];
       }
     }
+  }
+  template <int K, int L>
+  __device__ __forceinline__ static void fold_vecs(Lane (&acc)[L], const T (&x)[K][L], uint32_t step0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) fold_vec(acc, x[k], step0 + k);
   }
   template <int L, class Fn>
   __device__ __forceinline__ static typename OpT::Acc finish(const Lane (&acc)[L], Fn index_of) {

@@ -60,6 +60,42 @@ def tree_results(values, op, prec):
     return R[(1 << n) - 1]
 
 
+def mixed_tree_results(values, prec):
+    """Set of float sums over all binary trees whose every node is rounded EITHER to the
+    element precision OR kept in the library's wide accumulator (fp64 for float32 data;
+    double-double, exact at n <= 8 up to ~2^-100 relative, for float64 data), the root then
+    rounded once to the element precision -- the results the default float sum can give
+    (include/b200reduce.h: input-precision block trees added into a wide accumulator).
+    n <= 8; NaN-free finite inputs."""
+    n = len(values)
+    assert 1 <= n <= 8
+
+    def narrow(v):
+        if prec == "float32":
+            return Fraction(float(np.float32(float(v))))
+        return Fraction(float(v))            # Fraction -> nearest double (correctly rounded)
+
+    def wide(v):
+        return Fraction(float(v)) if prec == "float32" else v   # fp64 rounding / exact
+
+    R = {1 << i: {Fraction(float(v))} for i, v in enumerate(values)}
+    for mask in range(1, 1 << n):
+        if mask in R:
+            continue
+        low = mask & -mask
+        out = set()
+        sub = (mask - 1) & mask
+        while sub:
+            if sub & low and mask ^ sub:
+                for a in R[sub]:
+                    for b in R[mask ^ sub]:
+                        out.add(narrow(a + b))
+                        out.add(wide(a + b))
+            sub = (sub - 1) & mask
+        R[mask] = out
+    return {float(narrow(v)) for v in R[(1 << n) - 1]}
+
+
 def int_exact(values, op, dtype):
     """Exact integer reduction with Python big ints, reduced mod 2^w (two's complement)."""
     w = WIDTH[dtype]

