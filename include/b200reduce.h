@@ -23,7 +23,10 @@
  *    (a cudaStream_t; NULL = the legacy default stream). They never
  *    synchronise the host and are capturable in CUDA graphs once the
  *    per-(device, stream) workspace exists (it is created by the first call
- *    on that stream, outside capture).
+ *    on that stream, outside capture). A captured graph keeps the capture
+ *    stream's workspace: do not replay it concurrently with other calls that
+ *    use that workspace (eager calls on the capture stream, or another graph
+ *    captured on the same stream) -- they would share one ticket.
  *  - Element-aligned base pointers are required (x % sizeof(dtype) == 0,
  *    else RD_ERR_MISALIGNED); any element offset is valid.
  *  - Bitwise ops (AND/OR/XOR) on float dtypes -> RD_ERR_UNSUPPORTED.
@@ -246,10 +249,15 @@ rd_status rd_shard_range(uint64_t n, int nranks, int rank, uint64_t* begin, uint
  * reduce_fused -- the sharded reduction with the exchange step INSIDE the
  * reduce kernel: the last CTA of rank r stores its rd_record into slot r of
  * every rank's mailbox over NVLink (peer stores to CUDA-IPC-mapped device
- * memory), publishes it with a system-scope release, waits for the W records
- * of this call in its own mailbox and folds them in rank order. One kernel
- * launch per rank; no NCCL call, no host synchronisation. Same results and
- * contract as reduce_multi (bitwise-identical on all ranks).
+ * memory) as self-validating "LL" words -- each 8-byte store carries 4
+ * payload bytes and the call's 32-bit epoch, so no fence or release is
+ * needed: a reader polls until every word carries the epoch -- waits for the
+ * W records of this call in its own mailbox and folds them in rank order.
+ * One kernel launch per rank; no NCCL call, no host synchronisation. Same
+ * results and contract as reduce_multi (bitwise-identical on all ranks).
+ * Every rank's record starts with the same 32-byte header {tag, 0, n} (exact
+ * sums add their words after it), so ranks that disagree on dtype or op --
+ * plain or exact -- report RD_ERR_MISMATCH, not a timeout.
  *
  * Setup (collective, every rank in the same order):
  *   rd_fused_create(&f, nranks, rank, device, handle)   allocates this rank's
@@ -258,7 +266,11 @@ rd_status rd_shard_range(uint64_t n, int nranks, int rank, uint64_t* begin, uint
  *   rd_fused_connect(f, handles)                         opens the peers'.
  * Single-process use (several virtual ranks, one or more devices):
  *   rd_fused_mailbox(f, &ptr) and rd_fused_connect_local(f, ptrs) with the
- *   nranks mailbox device pointers instead of IPC handles.
+ *   nranks mailbox device pointers instead of IPC handles; peer access from
+ *   this rank's device to every other mailbox's device is enabled there
+ *   (RD_ERR_UNSUPPORTED if the devices cannot access each other).
+ * rd_comm_init / rd_fused_create / rd_fused_connect* leave the caller's
+ * current device unchanged and synchronise no other stream.
  * Every rank must call reduce_fused the same number of times in the same
  * order (epochs are counted on the device, in each rank's mailbox, so the
  * call can be captured in a CUDA graph and replayed); nranks <= 32. A peer that

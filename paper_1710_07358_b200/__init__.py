@@ -310,6 +310,7 @@ class Comm:
     def check(self, stream=None):
         torch = _torch()
         st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        st = st.cuda_stream if hasattr(st, "cuda_stream") else st
         check(lib().rd_comm_check(self.handle, st), "rd_comm_check")
 
     def destroy(self):
@@ -378,10 +379,14 @@ class FusedComm:
         return comm
 
     @classmethod
-    def local(cls, nranks: int, device: int = 0) -> list:
+    def local(cls, nranks: int, device: int = 0, devices=None) -> list:
         """nranks virtual ranks in this process (tests, or several devices driven
-        by one process): mailboxes are connected by device pointer."""
-        comms = [cls._create(nranks, r, device, False)[0] for r in range(nranks)]
+        by one process): mailboxes are connected by device pointer; rank r's
+        mailbox lives on devices[r] (default: all on `device`)."""
+        devs = list(devices) if devices is not None else [device] * nranks
+        if len(devs) != nranks:
+            raise ValueError("devices must list one device per rank")
+        comms = [cls._create(nranks, r, devs[r], False)[0] for r in range(nranks)]
         ptrs = (ctypes.c_void_p * nranks)()
         for r, c in enumerate(comms):
             p = ctypes.c_void_p()

@@ -12,6 +12,8 @@
                                             building it is not using it)
 - tools/libprobe.so                         the HBM read-bandwidth probe (measurement
                                             tooling: bench.py's same-run read ceiling)
+- tools/libcubref.so                        CUB DeviceReduce::Reduce (bench.py's library
+                                            context row; never on the product path)
 """
 from __future__ import annotations
 
@@ -92,6 +94,17 @@ def build_probe(force: bool = False) -> str:
     return out
 
 
+def build_cub_ref(force: bool = False) -> str:
+    """tools/libcubref.so: CUB DeviceReduce::Reduce, bench.py's library context row."""
+    src = os.path.join(ROOT, "tools", "cub_ref.cu")
+    out = os.path.join(ROOT, "tools", "libcubref.so")
+    if force or _stale(out, [src]):
+        subprocess.check_call(["nvcc", *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+                               src, "-o", out + ".tmp"])
+        os.replace(out + ".tmp", out)
+    return out
+
+
 def build_all(force: bool = False) -> None:
     sys.path.insert(0, ROOT)
     import inputs
@@ -99,7 +112,7 @@ def build_all(force: bool = False) -> None:
     with cf.ThreadPoolExecutor(max_workers=4) as ex:
         futs = [ex.submit(build_library, force), ex.submit(inputs.build_device, force),
                 ex.submit(inputs.build_host, force), ex.submit(oracle.build, force),
-                ex.submit(build_probe, force)]
+                ex.submit(build_probe, force), ex.submit(build_cub_ref, force)]
         for f in futs:
             f.result()
 

@@ -576,6 +576,7 @@ rd_status launch_combine(const rd_record* recs, int count, int dtype, int op, vo
   if ((uintptr_t)recs % 16) { set_error("recs must be 16-byte aligned"); return RD_ERR_MISALIGNED; }
   if (out == nullptr && rec_out == nullptr) { set_error("no output"); return RD_ERR_INVALID_ARG; }
   if (out && (uintptr_t)out % (is_arg_op(op) ? 8 : dtype_size(dtype))) { set_error("out misaligned"); return RD_ERR_MISALIGNED; }
+  if (rec_out && (uintptr_t)rec_out % 16) { set_error("rec_out must be 16-byte aligned"); return RD_ERR_MISALIGNED; }
   CombineFn fn = lookup_combine(dtype, op);
   if (!fn) { set_error("no combine kernel"); return RD_ERR_UNSUPPORTED; }
   fn<<<1, 32, 0, stream>>>(recs, count, record_tag(dtype, op), out, rec_out, d_status);

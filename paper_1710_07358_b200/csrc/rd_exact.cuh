@@ -484,12 +484,32 @@ __device__ __noinline__ void exact_fused_exchange(long long* words, unsigned fla
     const unsigned long long v = (unsigned long long)words[(k - 4) >> 1];
     return (k & 1) ? (uint32_t)(v >> 32) : (uint32_t)v;
   };
+  // the common 32-byte LL header {tag, 0, n lo, n hi, 0...} goes through the
+  // same ll slots as every plain record, so a peer that runs another op or
+  // dtype (plain or exact) sees this tag and reports RD_ERR_MISMATCH instead
+  // of waiting for words it would never receive
   for (int p = 0; p < W; ++p) {
     volatile unsigned long long* dst = args.peers[p]->xll[par][args.rank];
     for (int k = ln; k < NP; k += 32) dst[k] = eflag | payload(k);   // peer stores over NVLink
+    if (ln < 8) {
+      const uint32_t h = ln == 0 ? args.tag : ln == 2 ? (uint32_t)args.n : ln == 3 ? (uint32_t)(args.n >> 32) : 0u;
+      args.peers[p]->ll[par][args.rank][ln] = eflag | h;
+    }
   }
-  bool timeout = false;
-  for (int q = 0; q < W && !timeout; ++q) {
+  bool timeout = false, bad = false;
+  for (int q = ln; q < W; q += 32) {                 // the peers' headers first
+    const volatile unsigned long long* src = args.self->ll[par][q];
+    uint32_t spins = 0;
+    unsigned long long v;
+    while (((v = src[0]) & 0xffffffff00000000ull) != eflag) {
+      if (++spins > 4096) __nanosleep(128);
+      if (spins > (1u << 25)) { timeout = true; break; }
+    }
+    bad |= !timeout && (uint32_t)v != args.tag;
+  }
+  timeout = __any_sync(0xffffffffu, timeout);
+  bad = __any_sync(0xffffffffu, bad);
+  for (int q = 0; q < W && !timeout && !bad; ++q) {
     const volatile unsigned long long* src = args.self->xll[par][q];
     for (int k = ln; k < NP; k += 32) {
       uint32_t spins = 0;
@@ -503,10 +523,9 @@ __device__ __noinline__ void exact_fused_exchange(long long* words, unsigned fla
   }
   __syncwarp();
   // every word of every record is in: sum them (lane j: words j, j+32, ...)
-  bool bad = false;
   unsigned long long n = 0;
   unsigned fl = 0;
-  if (!timeout) {
+  if (!timeout && !bad) {
     for (int q = 0; q < W; ++q) {
       const volatile unsigned long long* src = args.self->xll[par][q];
       bad |= (uint32_t)src[0] != args.tag;

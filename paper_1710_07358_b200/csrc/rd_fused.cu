@@ -22,9 +22,30 @@ struct rd_fused {
 };
 
 namespace {
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { if (cudaGetDevice(&prev) != cudaSuccess) prev = -1; }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+// zero / fill device memory without synchronising the device or the legacy
+// stream (other streams, e.g. the ranks of a running exchange, may be busy):
+// a private non-blocking stream, waited for alone
+cudaError_t private_copy(void* dst, const void* src, size_t bytes) {
+  cudaStream_t s;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return e;
+  e = src ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s) : cudaMemsetAsync(dst, 0, bytes, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  return e != cudaSuccess ? e : e2;
+}
+cudaError_t zero_sync(void* p, size_t bytes) { return private_copy(p, nullptr, bytes); }
+
 rd_status upload_peers(rd_fused* f, const std::vector<rd::Mailbox*>& ptrs) {
-  cudaError_t e = cudaMemcpy(f->d_peers, ptrs.data(), sizeof(rd::Mailbox*) * f->nranks, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemcpy(peers)");
+  cudaError_t e = private_copy(f->d_peers, ptrs.data(), sizeof(rd::Mailbox*) * f->nranks);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "copy of the peer table");
   // no lazy kernel loading once ranks may be spinning (rd_api.cu)
   rd_status st = rd::preload_default_kernels(f->device);
   if (st != RD_OK) return st;
@@ -40,6 +61,7 @@ rd_status rd_fused_create(rd_fused_t* out, int nranks, int rank, int device, voi
     rd::set_error("bad rd_fused_create arguments (nranks <= 32)");
     return RD_ERR_INVALID_ARG;
   }
+  DeviceGuard guard;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return rd::cuda_fail(e, "cudaSetDevice");
   rd_fused* f = new rd_fused();
@@ -49,9 +71,8 @@ rd_status rd_fused_create(rd_fused_t* out, int nranks, int rank, int device, voi
   void* p = nullptr;
   const size_t bytes = sizeof(rd::Mailbox) + 256;
   e = cudaMalloc(&p, bytes);
-  if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = zero_sync(p, bytes);
   if (e == cudaSuccess) e = cudaMalloc((void**)&f->d_peers, sizeof(rd::Mailbox*) * rd::kMaxRanks);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { cudaFree(p); delete f; return rd::cuda_fail(e, "mailbox allocation"); }
   f->self = (rd::Mailbox*)p;
   f->d_err = (int*)((char*)p + sizeof(rd::Mailbox));
@@ -68,6 +89,7 @@ rd_status rd_fused_create(rd_fused_t* out, int nranks, int rank, int device, voi
 
 rd_status rd_fused_connect(rd_fused_t f, const void* ipc_handles) {
   if (!f || !ipc_handles) { rd::set_error("bad rd_fused_connect arguments"); return RD_ERR_INVALID_ARG; }
+  DeviceGuard guard;
   cudaError_t e = cudaSetDevice(f->device);
   if (e != cudaSuccess) return rd::cuda_fail(e, "cudaSetDevice");
   std::vector<rd::Mailbox*> ptrs(f->nranks);
@@ -98,8 +120,31 @@ rd_status rd_fused_connect_local(rd_fused_t f, void* const* mailboxes) {
     ptrs[p] = (rd::Mailbox*)mailboxes[p];
   }
   if (ptrs[f->rank] != f->self) { rd::set_error("mailboxes[rank] is not this rank's mailbox"); return RD_ERR_INVALID_ARG; }
+  DeviceGuard guard;
   cudaError_t e = cudaSetDevice(f->device);
   if (e != cudaSuccess) return rd::cuda_fail(e, "cudaSetDevice");
+  // mailboxes on other devices are written by this rank's kernel (peer stores):
+  // peer access from this device to each of them must be enabled
+  for (int p = 0; p < f->nranks; ++p) {
+    cudaPointerAttributes pa;
+    e = cudaPointerGetAttributes(&pa, ptrs[p]);
+    if (e != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      rd::set_error("mailbox is not device memory");
+      return RD_ERR_INVALID_ARG;
+    }
+    if (pa.device == f->device) continue;
+    int can = 0;
+    e = cudaDeviceCanAccessPeer(&can, f->device, pa.device);
+    if (e != cudaSuccess) return rd::cuda_fail(e, "cudaDeviceCanAccessPeer");
+    if (!can) {
+      rd::set_error("no peer access between the devices of two mailboxes");
+      return RD_ERR_UNSUPPORTED;
+    }
+    e = cudaDeviceEnablePeerAccess(pa.device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();   // already on: fine
+    else if (e != cudaSuccess) return rd::cuda_fail(e, "cudaDeviceEnablePeerAccess");
+  }
   return upload_peers(f, ptrs);
 }
 
@@ -119,13 +164,15 @@ rd_status reduce_fused(const void* x_local, size_t n_local, rd_dtype dtype, rd_o
 
 rd_status rd_fused_check(rd_fused_t f, rd_stream_t stream) {
   if (!f) { rd::set_error("fused communicator is NULL"); return RD_ERR_INVALID_ARG; }
-  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
-  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaStreamSynchronize");
+  // stream-ordered read-back and clear (no legacy-stream or device-wide sync)
   int h = 0;
-  e = cudaMemcpy(&h, f->d_err, sizeof(int), cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemcpy");
+  cudaError_t e = cudaMemcpyAsync(&h, f->d_err, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemcpyAsync");
+  e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaStreamSynchronize");
   if (h) {
-    cudaMemset(f->d_err, 0, sizeof(int));
+    e = cudaMemsetAsync(f->d_err, 0, sizeof(int), (cudaStream_t)stream);
+    if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemsetAsync");
     rd::set_error(h == RD_ERR_TIMEOUT ? "a peer's record never arrived" : "ranks disagree on dtype/op");
     return (rd_status)h;
   }
@@ -134,8 +181,9 @@ rd_status rd_fused_check(rd_fused_t f, rd_stream_t stream) {
 
 rd_status rd_fused_destroy(rd_fused_t f) {
   if (!f) { rd::set_error("fused communicator is NULL"); return RD_ERR_INVALID_ARG; }
+  DeviceGuard guard;
   cudaSetDevice(f->device);
-  cudaDeviceSynchronize();
+  cudaDeviceSynchronize();   // no call of this communicator may still be in flight
   for (void* q : f->opened) cudaIpcCloseMemHandle(q);
   cudaFree(f->d_peers);
   cudaFree(f->self);

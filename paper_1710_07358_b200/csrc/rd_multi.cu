@@ -32,6 +32,25 @@ rd_status nccl_fail(ncclResult_t r, const char* what) {
   rd::set_error(std::string(what) + ": " + ncclGetErrorString(r));
   return RD_ERR_NCCL;
 }
+
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { if (cudaGetDevice(&prev) != cudaSuccess) prev = -1; }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+// zero device memory on a private stream and wait for that stream only (no
+// device-wide synchronisation: other streams may hold running work)
+cudaError_t zero_sync(void* p, size_t bytes) {
+  cudaStream_t s;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(p, 0, bytes, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  return e != cudaSuccess ? e : e2;
+}
 }  // namespace
 
 extern "C" {
@@ -50,6 +69,7 @@ rd_status rd_comm_init(rd_comm_t* comm, int nranks, int rank, const rd_unique_id
     rd::set_error("bad rd_comm_init arguments");
     return RD_ERR_INVALID_ARG;
   }
+  DeviceGuard guard;                    // the caller's current device is restored
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return rd::cuda_fail(e, "cudaSetDevice");
   rd_comm* c = new rd_comm();
@@ -63,16 +83,14 @@ rd_status rd_comm_init(rd_comm_t* comm, int nranks, int rank, const rd_unique_id
   void* p = nullptr;
   e = cudaMalloc(&p, sizeof(rd_record) * (nranks + 1) + 64);
   if (e != cudaSuccess) { ncclCommDestroy(c->nccl); delete c; return rd::cuda_fail(e, "cudaMalloc"); }
-  e = cudaMemset(p, 0, sizeof(rd_record) * (nranks + 1) + 64);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  e = zero_sync(p, sizeof(rd_record) * (nranks + 1) + 64);
   if (e != cudaSuccess) { cudaFree(p); ncclCommDestroy(c->nccl); delete c; return rd::cuda_fail(e, "comm buffers"); }
   c->d_send = (rd_record*)p;
   c->d_recv = c->d_send + 1;
   c->d_err = (int*)(c->d_recv + nranks);
   void* q = nullptr;
   e = cudaMalloc(&q, sizeof(rd_exact_record) * (nranks + 1));
-  if (e == cudaSuccess) e = cudaMemset(q, 0, sizeof(rd_exact_record) * (nranks + 1));
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = zero_sync(q, sizeof(rd_exact_record) * (nranks + 1));
   if (e != cudaSuccess) {
     if (q) cudaFree(q);
     cudaFree(p);
@@ -88,8 +106,9 @@ rd_status rd_comm_init(rd_comm_t* comm, int nranks, int rank, const rd_unique_id
 
 rd_status rd_comm_destroy(rd_comm_t comm) {
   if (!comm) { rd::set_error("comm is NULL"); return RD_ERR_INVALID_ARG; }
+  DeviceGuard guard;
   cudaSetDevice(comm->device);
-  cudaDeviceSynchronize();
+  cudaDeviceSynchronize();   // no call of this communicator may still be in flight
   ncclResult_t r = ncclCommDestroy(comm->nccl);
   cudaFree(comm->d_send);
   cudaFree(comm->d_xsend);
@@ -134,13 +153,15 @@ rd_status reduce_multi(const void* x_local, size_t n_local, rd_dtype dtype, rd_o
 
 rd_status rd_comm_check(rd_comm_t comm, rd_stream_t stream) {
   if (!comm) { rd::set_error("comm is NULL"); return RD_ERR_INVALID_ARG; }
-  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
-  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaStreamSynchronize");
+  // stream-ordered read-back and clear (no legacy-stream or device-wide sync)
   int h = 0;
-  e = cudaMemcpy(&h, comm->d_err, sizeof(int), cudaMemcpyDeviceToHost);
-  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemcpy");
+  cudaError_t e = cudaMemcpyAsync(&h, comm->d_err, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemcpyAsync");
+  e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return rd::cuda_fail(e, "cudaStreamSynchronize");
   if (h) {
-    cudaMemset(comm->d_err, 0, sizeof(int));
+    e = cudaMemsetAsync(comm->d_err, 0, sizeof(int), (cudaStream_t)stream);
+    if (e != cudaSuccess) return rd::cuda_fail(e, "cudaMemsetAsync");
     rd::set_error("ranks disagree on dtype/op");
     return RD_ERR_MISMATCH;
   }

@@ -20,7 +20,7 @@ def _run(*args):
 
 
 def test_bench_line_contract():
-    d = _run("--steps", "20", "--warmup", "3", "--log2n", "26", "--cpu-seconds", "0.5")
+    d = _run("--steps", "20", "--warmup", "3", "--log2n", "26", "--cpu-seconds", "0.5", "--c5-log2n", "27")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
               "gpu_launches", "clocks"):
@@ -34,10 +34,22 @@ def test_bench_line_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == (1 << 26) * 4 and e["d2h_bytes_per_step"] == 4
     assert "workload" in d["config"]
+    ctx = d["context"]
+    assert ctx["check"]["ok"] is True and ctx["check"]["err_over_bound"] < 1   # the timed result vs the oracle
+    assert ctx["int32_sum"]["check_bit_exact"] is True and ctx["int32_sum"]["gbs"] > 100
+    assert ctx["cub_device_reduce_gbs"] > 100 and ctx["torch_sum_gbs"] > 100
+    assert 0.5 < r["frac_of_read_probe"] < 1.2 and d["pct_read_probe"] > 50
+    c5 = ctx["c5"]
+    assert c5["n_total"] == 1 << 27 and c5["ranks"] == 1 and "fused_error" not in c5
+    for k in ("sum_nccl_gbs", "sum_fused_gbs", "max_nccl_gbs", "max_fused_gbs"):
+        assert c5[k] > 100, k
+    assert c5["check"]["max_is_planted"] and c5["check"]["fused_equals_nccl"] and c5["check"]["sum_within_bound"]
 
 
 def test_bench_force_comm_paths():
     for exch in ("fused", "nccl"):
-        d = _run("--steps", "10", "--warmup", "3", "--log2n", "24", "--no-cpu", "--force-comm", "--exchange", exch)
+        d = _run("--steps", "10", "--warmup", "3", "--log2n", "24", "--no-cpu", "--force-comm", "--exchange", exch,
+                 "--no-c5")
         assert d["value"] > 100
+        assert d["context"]["check"]["ok"] is True
         assert ("fused" in d["config"]["exchange"]) == (exch == "fused")
