@@ -408,6 +408,64 @@ __device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L
   }
 }
 
+// fp32 data, the per-element path for one group whose group speculation
+// failed, out of line (one copy per kernel): fold_vec_exact's levels --
+// tested adds into a0, then two TwoSum levels, then the element replay.
+template <int E, int GL>
+__device__ __noinline__ ExState<E, GL> exact32_elementwise(ExState<E, GL> st, const ExVals<GL> xs, long long* w) {
+  fold_vec_exact<float, E, GL>(st.ex, xs.v, w, st.flags);
+  return st;
+}
+
+// fp32 data, a GROUP of GL elements (one LDG.256, or two LDS.128 of the bulk
+// ring): each element is m * 2^(e-150) with m < 2^24, so when the group's
+// exponent fields span at most 29 - log2(GL) (zeros excluded), every partial
+// sum of the group is an integer multiple of 2^(e_min-150) below
+// 2^(53+e_min-150): the group's fp64 tree sum is EXACT whatever the order.
+// Then ONE tested add puts it into a0 (fl(t - a0) == s && fl(t - s) == a0,
+// as in fold_vec_exact). Per element: the F2F widening, 7/8 DADD and 4
+// integer ops (|b|, max |b|, |b| - 1, min) -- 1.5 FP64 ops per element
+// instead of the per-element test's 5: the FP64 work and its power were
+// what held the sustained exact sum at 85% of the read probe.
+// The max |b| < inf test sends inf/NaN groups, the e_min (from |b| - 1, so
+// zeros drop out and subnormals count as exponent 0) test wide or subnormal
+// groups, and an inexact add into a0 any group, to the per-element path.
+template <int E, int GL>
+__device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], int g, const uint32_t (&b)[GL], long long* w,
+                                                   uint32_t& flags) {
+  static_assert(GL == 4 || GL == 8 || GL == 16, "group of 4, 8 or 16 floats");
+  constexpr int kMaxSpread = 29 - (GL == 4 ? 2 : GL == 8 ? 3 : 4);
+  uint32_t mx = 0, mn = 0xffffffffu;
+  double x[GL];
+#pragma unroll
+  for (int l = 0; l < GL; ++l) {
+    const uint32_t a = b[l] & 0x7fffffffu;
+    mx = max(mx, a);
+    mn = min(mn, a - 1u);                            // zero -> 0xffffffff: no effect
+    x[l] = (double)__uint_as_float(b[l]);            // exact widening
+  }
+  const double s = tree_sum<GL>(x);                  // exact when the spread test holds
+  Ex& q = ex[g % E];
+  const double t = __dadd_rn(q.a0, s);
+  const bool bad = (mx >= 0x7f800000u) | ((int)(mx >> 23) - (int)(mn >> 23) > kMaxSpread) |
+                   (__dsub_rn(t, q.a0) != s) | (__dsub_rn(t, s) != q.a0);
+  if (__builtin_expect(!__any_sync(__activemask(), bad), 1)) {
+    q.a0 = t;
+    return;
+  }
+  ExState<E, GL> st;
+#pragma unroll
+  for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
+  st.flags = flags;
+  ExVals<GL> v;
+#pragma unroll
+  for (int l = 0; l < GL; ++l) v.v[l] = x[l];
+  st = exact32_elementwise<E, GL>(st, v, w);
+#pragma unroll
+  for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
+  flags = st.flags;
+}
+
 // round the normalised words (value = sum w[k] 2^(32k) * 2^kLsb) once; returns the float's bits
 template <typename T>
 __device__ uint64_t exact_round(const long long* w, uint32_t flags, uint64_t n) {
@@ -811,19 +869,27 @@ __device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E]
     for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      double xs[L];
+      if constexpr (sizeof(T) == 4) {
+        fold_group_exact32<E, L>(ex, u, v[u].w, w, flags);
+      } else {
+        double xs[L];
 #pragma unroll
-      for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v[u], l));
-      fold_vec_exact<T, E, L>(ex, xs, w, flags);
+        for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v[u], l));
+        fold_vec_exact<T, E, L>(ex, xs, w, flags);
+      }
     }
     __syncwarp();
   }
   for (; i < nvec; i += stride) {
     Vec<VB> v = ldg_stream<VB>(body + i * VB);
-    double xs[L];
+    if constexpr (sizeof(T) == 4) {
+      fold_group_exact32<E, L>(ex, 0, v.w, w, flags);
+    } else {
+      double xs[L];
 #pragma unroll
-    for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v, l));
-    fold_vec_exact<T, E, L>(ex, xs, w, flags);
+      for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v, l));
+      fold_vec_exact<T, E, L>(ex, xs, w, flags);
+    }
   }
   pdl_trigger();
   // a2: head and tail stragglers
@@ -951,13 +1017,22 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
         uint4 v[PER_THREAD];
 #pragma unroll
         for (int k = 0; k < PER_THREAD; ++k) v[k] = lds128(base + (k * CT + t) * 16);
+        if constexpr (sizeof(T) == 4 && PER_THREAD % 2 == 0) {
+          // fp32: groups of 8 (two LDS.128), one tested add per group
 #pragma unroll
-        for (int k = 0; k < PER_THREAD; ++k) {
-          Vec<16> q{{v[k].x, v[k].y, v[k].z, v[k].w}};
-          double xs[L];
+          for (int k = 0; k < PER_THREAD; k += 2) {
+            const uint32_t b8[8] = {v[k].x, v[k].y, v[k].z, v[k].w, v[k + 1].x, v[k + 1].y, v[k + 1].z, v[k + 1].w};
+            fold_group_exact32<E, 8>(ex, k / 2, b8, w, flags);
+          }
+        } else {
 #pragma unroll
-          for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, 16>(q, l));
-          fold_vec_exact<T, E, L>(ex, xs, w, flags);
+          for (int k = 0; k < PER_THREAD; ++k) {
+            Vec<16> q{{v[k].x, v[k].y, v[k].z, v[k].w}};
+            double xs[L];
+#pragma unroll
+            for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, 16>(q, l));
+            fold_vec_exact<T, E, L>(ex, xs, w, flags);
+          }
         }
       } else {
         for (int k = 0; k < PER_THREAD; ++k) {
