@@ -51,11 +51,12 @@ def _stale(out, srcs):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def _compile(src: str, force: bool, tuning: bool = False) -> str:
-    obj = os.path.join(TUNING_OBJ if tuning else OBJ, os.path.basename(src).replace(".cu", ".o"))
+def _compile(src: str, force: bool, tuning: bool = False, defines=(), objdir=None) -> str:
+    objdir = objdir or (TUNING_OBJ if tuning else OBJ)
+    obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
     if force or _stale(obj, [src] + _deps()):
         cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               *(["-DRD_TUNING"] if tuning else []),
+               *(["-DRD_TUNING"] if tuning else []), *[f"-D{d}" for d in defines],
                "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(nccl_dir(), "include"),
                "-c", src, "-o", obj + ".tmp"]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -67,13 +68,16 @@ def _compile(src: str, force: bool, tuning: bool = False) -> str:
     return obj
 
 
-def build_library(force: bool = False, tuning: bool = False) -> str:
-    lib = TUNING_LIB if tuning else LIB
-    os.makedirs(TUNING_OBJ if tuning else OBJ, exist_ok=True)
+def build_library(force: bool = False, tuning: bool = False, defines=(), out: str | None = None) -> str:
+    """The product library; `tuning` or `defines` + `out`: a measurement build
+    of the same sources (A/B of design alternatives, tools/ab_lib.py)."""
+    lib = out or (TUNING_LIB if tuning else LIB)
+    objdir = (os.path.join(os.path.dirname(lib), "obj") if out else (TUNING_OBJ if tuning else OBJ))
+    os.makedirs(objdir, exist_ok=True)
     os.makedirs(os.path.dirname(lib), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=max(2, os.cpu_count() or 2)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, tuning), srcs))
+        objs = list(ex.map(lambda s: _compile(s, force, tuning, defines, objdir), srcs))
     if force or _stale(lib, objs):
         nd = nccl_dir()
         cmd = ["nvcc", *ARCH, "-shared", "-o", lib + ".tmp", *objs,
@@ -118,7 +122,11 @@ def build_all(force: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    if "--tuning" in sys.argv:
+    if "--define" in sys.argv:     # A/B build: --define NAME --out build/ab/x/libb200reduce.so
+        d = sys.argv[sys.argv.index("--define") + 1]
+        o = os.path.abspath(sys.argv[sys.argv.index("--out") + 1])
+        print(build_library(force="--force" in sys.argv, defines=(d,), out=o))
+    elif "--tuning" in sys.argv:
         print(build_library(force="--force" in sys.argv, tuning=True))
     else:
         build_all(force="--force" in sys.argv)

@@ -564,39 +564,17 @@ struct LaneOps<OpT, true> {
   struct Lane { T key; uint32_t step; };
   static constexpr uint32_t kEmpty = 0xffffffffu;
   __device__ __forceinline__ static Lane identity() { return Lane{OpT::identity().key, kEmpty}; }
+#ifdef RD_ARG_PER_LANE
+  // (A/B builds only) one (key, step) per lane: L independent select chains
   template <int L>
   __device__ __forceinline__ static void fold_vec(Lane (&acc)[L], const T (&x)[L], uint32_t step) {
-    // one (key, step) per lane: L independent chains.
-    if constexpr (OpT::kFloat) {   // +2-3% for float arg ops (A/B, one box)
-      // NaN test per PAIR of lanes (one unordered compare), not per element;
-      // only a vector holding a NaN takes the NaN-mapping path
-      const bool nan = any_nan<L>(x);
-      if (__builtin_expect(!nan, 1)) {
+    const bool nan = OpT::kFloat && any_nan<L>(x);
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-          const T k = OpT::raw_key(x[l]);
-          const bool better = OP_IS_MIN(OpT) ? (k < acc[l].key) : (k > acc[l].key);
-          acc[l] = better ? Lane{k, step} : acc[l];
-        }
-      } else {
-#pragma unroll
-        for (int l = 0; l < L; ++l) {
-          const T k = OpT::key_of(x[l]);
-          const bool better = OP_IS_MIN(OpT) ? (k < acc[l].key) : (k > acc[l].key);
-          acc[l] = better ? Lane{k, step} : acc[l];
-        }
-      }
-    } else {
-#pragma unroll
-      for (int l = 0; l < L; ++l) {
-        const T k = OpT::key_of(x[l]);
-        // integer keys can equal the identity key, so an empty lane takes its
-        // first element unconditionally (a later equal key never displaces an
-        // earlier one). [A lexicographic (key, step) compare measured slower.]
-        bool better = OP_IS_MIN(OpT) ? (k < acc[l].key) : (k > acc[l].key);
-        better = better || (acc[l].step == kEmpty);
-        acc[l] = better ? Lane{k, step} : acc[l];
-      }
+    for (int l = 0; l < L; ++l) {
+      const T k = nan ? OpT::key_of(x[l]) : OpT::raw_key(x[l]);
+      bool better = OP_IS_MIN(OpT) ? (k < acc[l].key) : (k > acc[l].key);
+      if constexpr (!OpT::kFloat) better = better || (acc[l].step == kEmpty);
+      acc[l] = better ? Lane{k, step} : acc[l];
     }
   }
   template <int K, int L>
@@ -612,6 +590,104 @@ struct LaneOps<OpT, true> {
       if (acc[l].step != kEmpty) a = OpT::combine(a, typename OpT::Acc{acc[l].key, index_of(acc[l].step, (uint32_t)l)});
     return a;
   }
+#else
+  // Group-best: ONE (key, position) per thread, in acc[0]. A group of G
+  // vectors (G*L <= 8 keys) is reduced to its best key by a min/max tree
+  // (IMNMX / VIMNMX3: no select chains), then compared once with the
+  // thread's best; only an improvement -- rare after the first groups, about
+  // ln(groups) times per thread -- takes the (divergent) branch that finds the
+  // group's FIRST position holding that key and records step * L + lane. A
+  // strict comparison keeps the earliest of equal keys across groups, the
+  // first position within one: the lowest index, as the per-lane form did, at
+  // ~3 integer ops per element instead of ~5 (sustained float32 argmax was
+  // 88.8% of the read probe, the lowest of all (dtype, op)).
+  template <int N>
+  __device__ __forceinline__ static T best_of(const T* k) {
+    if constexpr (N == 1) return k[0];
+    else {
+      const T a = best_of<N - N / 2>(k), b = best_of<N / 2>(k + (N - N / 2));
+      return OP_IS_MIN(OpT) ? (a < b ? a : b) : (a > b ? a : b);
+    }
+  }
+  using F = typename std::conditional<sizeof(T) == 4, float, double>::type;
+  __device__ __forceinline__ static F as_float(T b) {
+    if constexpr (sizeof(T) == 4) return __uint_as_float((uint32_t)b);
+    else return __longlong_as_double((long long)b);
+  }
+  template <int N>
+  __device__ __forceinline__ static F fbest_of(const T* x) {    // FMNMX / FMNMX3, DSETP.MAX
+    if constexpr (N == 1) return as_float(x[0]);
+    else {
+      const F a = fbest_of<N - N / 2>(x), b = fbest_of<N / 2>(x + (N - N / 2));
+      return OP_IS_MIN(OpT) ? fmin(a, b) : fmax(a, b);
+    }
+  }
+  template <int G, int L>
+  __device__ __forceinline__ static void fold_group(Lane& best, const T* x, uint32_t step0) {
+    constexpr int N = G * L;
+    bool nan = false;
+    if constexpr (OpT::kFloat) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) nan |= any_nan<L>(*reinterpret_cast<const T(*)[L]>(x + g * L));
+      // floats: the group's best by the float min/max instructions (1 op per
+      // element, no key transform); fmin/fmax return one of the operands, so
+      // its bits are an element's -- unless the best is a zero (-0 vs +0 are
+      // not ordered by fmin/fmax) or a NaN is present: then the key path below
+      const F m = fbest_of<N>(x);
+      if (__builtin_expect(!nan && m != (F)0, 1)) {
+        T mb;
+        if constexpr (sizeof(T) == 4) mb = (T)__float_as_uint(m);
+        else mb = (T)__double_as_longlong(m);
+        const T vb = OpT::raw_key(mb);
+        if (__builtin_expect(OP_IS_MIN(OpT) ? (vb < best.key) : (vb > best.key), 0)) {
+          uint32_t j0 = N - 1;
+#pragma unroll
+          for (int j = N - 1; j >= 0; --j) j0 = (x[j] == mb) ? (uint32_t)j : j0;
+          best.key = vb;
+          best.step = step0 * L + j0;
+        }
+        return;
+      }
+    }
+    T k[N];
+    if (__builtin_expect(!nan, 1)) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) k[j] = OpT::raw_key(x[j]);
+    } else {                                            // NaN maps to the winning end
+#pragma unroll
+      for (int j = 0; j < N; ++j) k[j] = OpT::key_of(x[j]);
+    }
+    const T vb = best_of<N>(k);
+    bool upd = OP_IS_MIN(OpT) ? (vb < best.key) : (vb > best.key);
+    // integer keys can equal the identity key: an empty thread takes its first group
+    if constexpr (!OpT::kFloat) upd = upd || (best.step == kEmpty);
+    if (__builtin_expect(upd, 0)) {
+      uint32_t j0 = N - 1;
+#pragma unroll
+      for (int j = N - 1; j >= 0; --j) j0 = (k[j] == vb) ? (uint32_t)j : j0;
+      best.key = vb;
+      best.step = step0 * L + j0;                       // = (step0 + j0 / L) * L + j0 % L
+    }
+  }
+  template <int L>
+  __device__ __forceinline__ static void fold_vec(Lane (&acc)[L], const T (&x)[L], uint32_t step) {
+    fold_group<1, L>(acc[0], x, step);
+  }
+  template <int K, int L>
+  __device__ __forceinline__ static void fold_vecs(Lane (&acc)[L], const T (&x)[K][L], uint32_t step0) {
+    constexpr int G0 = (L >= 8) ? 1 : 8 / L;
+    constexpr int G = (K % G0 == 0) ? G0 : 1;
+#pragma unroll
+    for (int k = 0; k < K; k += G) fold_group<G, L>(acc[0], &x[k][0], step0 + k);
+  }
+  template <int L, class Fn>
+  __device__ __forceinline__ static typename OpT::Acc finish(const Lane (&acc)[L], Fn index_of) {
+    typename OpT::Acc a = OpT::identity();
+    if (acc[0].step != kEmpty)
+      a = typename OpT::Acc{acc[0].key, index_of(acc[0].step / L, acc[0].step % L)};
+    return a;
+  }
+#endif
 };
 
 // ---------------------------------------------------------------- type map

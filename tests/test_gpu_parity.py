@@ -626,6 +626,47 @@ def test_arg_ops_special_values(rd, prec):
                     _parity.check(got, x, op)
 
 
+@pytest.mark.parametrize("prec", FLT)
+def test_arg_ops_group_ties_and_zeros(rd, prec):
+    """The group-best fold (rd_ops.cuh LaneOps): the best of a group of <= 8 elements by
+    FMNMX, an improvement located at the group's FIRST position holding it, ties kept at
+    the earliest group; a zero best (-0 vs +0, unordered by fmin/fmax) and NaN groups
+    take the key path. Ties inside one vector, across vectors of one group, across
+    groups of one thread and across threads, at every alignment, both variants."""
+    rng = np.random.default_rng(7)
+    n = 300007
+    cases = []
+    x = rng.uniform(-1, 1, n).astype(prec)
+    for pos in ([5, 6], [8, 15], [64, 65, 70], [1000, 1003, 200000], [n - 3, n - 1]):
+        y = x.copy()
+        y[pos] = 3.0                                  # the max, tied
+        z = y.copy()
+        z[pos] = -3.0                                 # the min, tied
+        cases += [y, z]
+    zeros = np.full(n, -1.0, dtype=prec)              # max is a zero: -0 at 10, +0 at 90000
+    zeros[10] = -0.0
+    zeros[90000] = 0.0
+    cases.append(zeros)
+    zneg = np.full(n, 1.0, dtype=prec)                # min is a zero: +0 at 7, -0 at 5000
+    zneg[7] = 0.0
+    zneg[5000] = -0.0
+    cases.append(zneg)
+    only_negz = np.full(n, -0.0, dtype=prec)          # every element -0: index 0
+    cases.append(only_negz)
+    mixed0 = np.where(rng.random(n) < 0.5, 0.0, -0.0).astype(prec)
+    cases.append(mixed0)
+    nan_late = x.copy()
+    nan_late[123456] = np.nan
+    nan_late[123457] = np.nan
+    cases.append(nan_late)
+    for c in cases:
+        for op in ("argmin", "argmax"):
+            for off in (0, 1, 3):
+                for variant in ("auto", "vector", "bulk"):
+                    got = val(rd.reduce_ex(to_dev(c, off), op, variant=variant)[0])
+                    _parity.check(got, c, op)
+
+
 @pytest.mark.parametrize("dtype", INT + FLT)
 def test_arg_ops_sharded_records(rd, dtype):
     """Shard records carry block-local indices; rd_combine_records shifts them by

@@ -14,9 +14,15 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 
 DT = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
-OPS = {"sum": 0, "max": 3, "argmin": 7, "argmax": 8, "sum_exact": 10}
+OPS = {"sum": 0, "max": 3, "argmin": 7, "argmax": 8, "sum_compensated": 9, "sum_exact": 10}
 PAIRS = [("float32", "argmin"), ("float32", "argmax"), ("int32", "argmax"), ("float64", "argmin"),
          ("float32", "sum"), ("int32", "sum"), ("float64", "max"), ("int64", "argmin"), ("uint32", "argmax")]
+if os.environ.get("AB_PAIRS"):            # e.g. AB_PAIRS=uint32:argmax,float32:argmin
+    PAIRS = [tuple(p.split(":")) for p in os.environ["AB_PAIRS"].split(",")]
+# AB_SOAK=S: S seconds of back-to-back calls before each timing (the sustained,
+# power-capped regime bench.py measures); AB_REPS: calls per timing
+SOAK = float(os.environ.get("AB_SOAK", "0"))
+REPS = int(os.environ.get("AB_REPS", "20"))
 if os.environ.get("AB_EXACT"):
     PAIRS.append(("float32", "sum_exact"))
 
@@ -33,15 +39,21 @@ def run(path, x_by_dtype):
         f = lambda: L.reduce(x.data_ptr(), x.numel(), DT[dtype], OPS[op], out.data_ptr(), st.cuda_stream)
         for _ in range(5):
             assert f() == 0
+        import time
+        t_end = time.perf_counter() + SOAK
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                f()
+            torch.cuda.synchronize()
         ts = []
         for _ in range(5):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(st)
-            for _ in range(20):
+            for _ in range(REPS):
                 f()
             b.record(st)
             b.synchronize()
-            ts.append(a.elapsed_time(b) / 20 * 1e-3)
+            ts.append(a.elapsed_time(b) / REPS * 1e-3)
         ts.sort()
         res[f"{dtype}-{op}"] = round(x.numel() * x.element_size() / ts[2] / 1e9, 1)
     return res
