@@ -466,6 +466,70 @@ __device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], int g, const uin
   flags = st.flags;
 }
 
+// fp64 data, the per-element path for one group (out of line)
+template <int E, int GL>
+__device__ __noinline__ ExState<E, GL> exact64_elementwise(ExState<E, GL> st, const ExVals<GL> xs, long long* w) {
+  fold_vec_exact<double, E, GL>(st.ex, xs.v, w, st.flags);
+  return st;
+}
+
+// fp64 data, a GROUP of GL elements into one expansion (a0, a1), speculating
+// on facts one integer bookkeeping pass per group proves:
+//  * Fast2Sum is exact: every running a0 has an exponent >= every x's
+//    (min |a0| hi word >= max |x| hi word), so a0 + x = s + e with
+//    e = x - (s - a0): 3 DADD instead of TwoSum's 6;
+//  * the GL errors sum exactly in a tree: each e is a multiple of ulp(x) >=
+//    2^(xmin - 1075) (a0 is a multiple of it too; if s lands below x's
+//    binade the add was exact, e = 0) and |e| <= ulp(s)/2 <= 2^(smax - 1076),
+//    so with smax - xmin <= 54 - log2(GL) every partial fits 53 bits;
+//  * ONE tested add puts the error sum into a1 (as spec2's test).
+// 3 + 7/8 + 5/8 FP64 ops per element instead of spec2's 11, plus 6 integer
+// ops (|hi|, max, min(|hi| - 1) for x; |hi|, min, max for a0). Overflow,
+// inf/NaN, a small running sum (|a0| below some |x|: every thread's first
+// group, sign changes of the sum), wide groups or an inexact a1 add: the
+// per-element levels, out of line.
+template <int E, int GL>
+__device__ __forceinline__ void fold_group_exact64(Ex (&ex)[E], int g, const double (&x)[GL], long long* w,
+                                                   uint32_t& flags) {
+  static_assert(GL == 4 || GL == 8, "group of 4 or 8 doubles");
+  constexpr int kMaxSpread = 54 - (GL == 4 ? 2 : 3);
+  Ex& q = ex[g % E];
+  uint32_t xmax = 0, xmin = 0xffffffffu, amin = 0xffffffffu, smax = 0;
+  double a = q.a0, e[GL];
+#pragma unroll
+  for (int l = 0; l < GL; ++l) {
+    const uint32_t xh = (uint32_t)__double2hiint(x[l]) & 0x7fffffffu;
+    xmax = max(xmax, xh);
+    xmin = min(xmin, xh - 1u);                       // zero -> 0xffffffff: no effect
+    amin = min(amin, (uint32_t)__double2hiint(a) & 0x7fffffffu);
+    const double sl = __dadd_rn(a, x[l]);
+    e[l] = __dsub_rn(x[l], __dsub_rn(sl, a));        // Fast2Sum
+    a = sl;
+    smax = max(smax, (uint32_t)__double2hiint(a) & 0x7fffffffu);
+  }
+  const double se = tree_sum<GL>(e);
+  const double t = __dadd_rn(q.a1, se);
+  const bool bad = (smax >= 0x7ff00000u) | (xmax >= 0x7ff00000u) | (amin < xmax) |
+                   ((int)(smax >> 20) - (int)(xmin >> 20) > kMaxSpread) |
+                   (__dsub_rn(t, q.a1) != se) | (__dsub_rn(t, se) != q.a1);
+  if (__builtin_expect(!__any_sync(__activemask(), bad), 1)) {
+    q.a0 = a;
+    q.a1 = t;
+    return;
+  }
+  ExState<E, GL> st;
+#pragma unroll
+  for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
+  st.flags = flags;
+  ExVals<GL> v;
+#pragma unroll
+  for (int l = 0; l < GL; ++l) v.v[l] = x[l];
+  st = exact64_elementwise<E, GL>(st, v, w);
+#pragma unroll
+  for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
+  flags = st.flags;
+}
+
 // round the normalised words (value = sum w[k] 2^(32k) * 2^kLsb) once; returns the float's bits
 template <typename T>
 __device__ uint64_t exact_round(const long long* w, uint32_t flags, uint64_t n) {
@@ -867,15 +931,28 @@ __device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E]
     Vec<VB> v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
+    if constexpr (sizeof(T) == 4) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if constexpr (sizeof(T) == 4) {
-        fold_group_exact32<E, L>(ex, u, v[u].w, w, flags);
-      } else {
+      for (int u = 0; u < U; ++u) fold_group_exact32<E, L>(ex, u, v[u].w, w, flags);
+    } else if constexpr (U % 2 == 0) {
+      // fp64: groups of 8 (two 32-byte vectors)
+#pragma unroll
+      for (int u = 0; u < U; u += 2) {
+        double xs[2 * L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          xs[l] = lane<T, VB>(v[u], l);
+          xs[L + l] = lane<T, VB>(v[u + 1], l);
+        }
+        fold_group_exact64<E, 2 * L>(ex, u / 2, xs, w, flags);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
         double xs[L];
 #pragma unroll
-        for (int l = 0; l < L; ++l) xs[l] = widen(lane<T, VB>(v[u], l));
-        fold_vec_exact<T, E, L>(ex, xs, w, flags);
+        for (int l = 0; l < L; ++l) xs[l] = lane<T, VB>(v[u], l);
+        fold_group_exact64<E, L>(ex, u, xs, w, flags);
       }
     }
     __syncwarp();
@@ -1023,6 +1100,19 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
           for (int k = 0; k < PER_THREAD; k += 2) {
             const uint32_t b8[8] = {v[k].x, v[k].y, v[k].z, v[k].w, v[k + 1].x, v[k + 1].y, v[k + 1].z, v[k + 1].w};
             fold_group_exact32<E, 8>(ex, k / 2, b8, w, flags);
+          }
+        } else if constexpr (sizeof(T) == 8 && PER_THREAD % 4 == 0) {
+          // fp64: groups of 8 (four LDS.128)
+#pragma unroll
+          for (int k = 0; k < PER_THREAD; k += 4) {
+            double d8[8];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              Vec<16> q{{v[k + j].x, v[k + j].y, v[k + j].z, v[k + j].w}};
+              d8[2 * j] = lane<T, 16>(q, 0);
+              d8[2 * j + 1] = lane<T, 16>(q, 1);
+            }
+            fold_group_exact64<E, 8>(ex, k / 4, d8, w, flags);
           }
         } else {
 #pragma unroll
