@@ -85,6 +85,21 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// RD_TIMELINE (measurement builds only, tools/timeline.py): %globaltimer
+// stamps per CTA -- entry, first full stage, stream end, ticket, and the last
+// CTA's fold / block reduce / output -- read back with rd_timeline_read.
+#ifdef RD_TIMELINE
+static __device__ unsigned long long rd_tl[4096][8];   // kMaxGrid CTAs
+__device__ __forceinline__ unsigned long long rd_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define RD_TL(slot) (rd_tl[blockIdx.x][slot] = rd_gtimer())
+#else
+#define RD_TL(slot) ((void)0)
+#endif
+
 template <int STAGES, int STAGE_BYTES, int CW>
 struct BulkSmem {
   static constexpr int kRing = STAGES * STAGE_BYTES;
@@ -125,6 +140,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   const unsigned char* body = args.x + args.head * sizeof(T);
   const uint64_t body_bytes = args.nvec * 16;
   pdl_wait();
+  if (threadIdx.x == 0) RD_TL(0);
 
   if (warp == CW) {
     // ---------------------------------------------------------------- producer
@@ -139,6 +155,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
       uint32_t next = atomicAdd(args.work, 1u) + gridDim.x;
       for (;; c = next, next = atomicAdd(args.work, 1u) + gridDim.x) {
         if (c >= args.nchunks) {
+          RD_TL(3);
           mbar_wait(&empty[stage], phase ^ 1);
           st_chunk[stage] = -1;
           mbar_arrive(&full[stage]);
@@ -171,10 +188,20 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
     uint32_t phase = 0, nchunk_local = 0;
     uint32_t cstage = 0;   // stage number within the current chunk
     const uint32_t ring_addr = smem_addr(ring);
+#ifdef RD_TIMELINE
+    bool first = true;
+#endif
     for (;;) {
       mbar_wait(&full[stage], phase);
+#ifdef RD_TIMELINE
+      if (first && t == 0) RD_TL(1);
+      first = false;
+#endif
       const int32_t c = st_chunk[stage];
-      if (c < 0) break;
+      if (c < 0) {
+        if (t == 0) RD_TL(2);
+        break;
+      }
       const uint32_t bytes = st_bytes[stage];
       const uint32_t last = st_last[stage];
       const uint32_t base = ring_addr + stage * STAGE_BYTES;
@@ -264,21 +291,25 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
     __threadfence();                                   // release this CTA's chunk partials
     const unsigned tk = atomicAdd(args.ticket, 1u);
     s_last = (tk == gridDim.x - 1);
+    RD_TL(4);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   Acc b = fold_slots<OpT, B>(args.partials, args.nchunks);
+  if (threadIdx.x == 0) RD_TL(5);
   if (threadIdx.x < args.head) b = fold_at<OpT>(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)), threadIdx.x);
   if (threadIdx.x < args.tail)
     b = fold_at<OpT>(b, ldg_scalar<T>(args.x + (args.tail_start + threadIdx.x) * sizeof(T)),
                      args.tail_start + threadIdx.x);
   b = block_reduce<OpT, B>(b, red);
   if (threadIdx.x == 0) {
+    RD_TL(6);
     *args.ticket = 0u;
     *args.work = 0u;
   }
   if (threadIdx.x < 32) finish_warp0<OpT>(b, args);
+  if (threadIdx.x == 0) RD_TL(7);
 }
 
 }  // namespace rd
