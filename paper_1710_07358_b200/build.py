@@ -122,10 +122,10 @@ def build_all(force: bool = False) -> None:
 
 
 if __name__ == "__main__":
-    if "--define" in sys.argv:     # A/B build: --define NAME --out build/ab/x/libb200reduce.so
+    if "--define" in sys.argv:     # A/B build: --define NAME[,NAME2] --out build/ab/x/libb200reduce.so
         d = sys.argv[sys.argv.index("--define") + 1]
         o = os.path.abspath(sys.argv[sys.argv.index("--out") + 1])
-        print(build_library(force="--force" in sys.argv, defines=(d,), out=o))
+        print(build_library(force="--force" in sys.argv, defines=tuple(d.split(",")), out=o))
     elif "--tuning" in sys.argv:
         print(build_library(force="--force" in sys.argv, tuning=True))
     else:

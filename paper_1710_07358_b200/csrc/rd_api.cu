@@ -232,6 +232,17 @@ rd_status preload_default_kernels(int dev) {
   return RD_OK;
 }
 
+#ifdef RD_TIMELINE
+// measurement builds only (tools/timeline.py): the bulk kernel's per-CTA
+// %globaltimer stamps, one device buffer for the process (current device)
+unsigned long long* timeline_buffer() {
+  static unsigned long long* buf = nullptr;
+  if (!buf && cudaMalloc(&buf, (size_t)kMaxGrid * 8 * sizeof(unsigned long long)) == cudaSuccess)
+    cudaMemset(buf, 0, (size_t)kMaxGrid * 8 * sizeof(unsigned long long));
+  return buf;
+}
+#endif
+
 // a0: validate, plan, launch.
 rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, void* out,
                         rd_record* rec, cudaStream_t stream, const rd_config* cfg,
@@ -371,6 +382,9 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     a.nranks = fused->nranks;
     a.rank = fused->rank;
   }
+#ifdef RD_TIMELINE
+  a.tl = timeline_buffer();
+#endif
 
   // programmatic dependent launch: the grid may be scheduled while the previous
   // kernel on the stream drains; the kernels call griddepcontrol.wait before
@@ -600,6 +614,17 @@ static void release_all_workspaces() {
 }  // namespace rd
 
 // ====================================================================== C ABI
+#ifdef RD_TIMELINE
+extern "C" int rd_timeline_read(void* host, int nctas) {
+  if (nctas > rd::kMaxGrid) nctas = rd::kMaxGrid;
+  return (int)cudaMemcpy(host, rd::timeline_buffer(), (size_t)nctas * 8 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost);
+}
+extern "C" int rd_timeline_clear(void) {
+  return (int)cudaMemset(rd::timeline_buffer(), 0, (size_t)rd::kMaxGrid * 8 * sizeof(unsigned long long));
+}
+#endif
+
 extern "C" {
 
 rd_status reduce(const void* x, size_t n, rd_dtype dtype, rd_op op, void* out, rd_stream_t stream) {

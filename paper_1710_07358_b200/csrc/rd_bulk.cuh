@@ -38,6 +38,35 @@ namespace rd {
 #define RD_RELEASE_FENCE() ((void)0)
 #endif
 
+// Releasing a stage: every consumer thread arrives on the stage's EMPTY
+// barrier itself (count 32 * CW), after reading the stage and its metadata,
+// so each reader's own arrive (release) orders its reads before the
+// producer's next write into the stage -- the form compute-sanitizer's
+// racecheck follows (0 hazards; lane 0 arriving for its warp after
+// __syncwarp, count CW, is correct too but racecheck does not see it as
+// ordering the other lanes' reads). An A/B of both (profiles/ab/
+// r02_ab_arrive_all.jsonl) shows no throughput difference;
+// RD_ARRIVE_WARP restores the per-warp arrive.
+#ifndef RD_ARRIVE_WARP
+#define RD_EMPTY_COUNT(CW) (32 * (CW))
+#define RD_RELEASE_STAGE(bar) \
+  do {                        \
+    __syncwarp();             \
+    RD_RELEASE_FENCE();       \
+    mbar_arrive(bar);         \
+  } while (0)
+#else
+#define RD_EMPTY_COUNT(CW) (CW)
+#define RD_RELEASE_STAGE(bar)        \
+  do {                               \
+    __syncwarp();                    \
+    if ((threadIdx.x & 31) == 0) {   \
+      RD_RELEASE_FENCE();            \
+      mbar_arrive(bar);              \
+    }                                \
+  } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -87,15 +116,14 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 
 // RD_TIMELINE (measurement builds only, tools/timeline.py): %globaltimer
 // stamps per CTA -- entry, first full stage, stream end, ticket, and the last
-// CTA's fold / block reduce / output -- read back with rd_timeline_read.
+// CTA's fold / block reduce / output -- read back with rd_timeline_read (rd_api.cu).
 #ifdef RD_TIMELINE
-static __device__ unsigned long long rd_tl[4096][8];   // kMaxGrid CTAs
 __device__ __forceinline__ unsigned long long rd_gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-#define RD_TL(slot) (rd_tl[blockIdx.x][slot] = rd_gtimer())
+#define RD_TL(slot) (args.tl[blockIdx.x * 8 + (slot)] = rd_gtimer())
 #else
 #define RD_TL(slot) ((void)0)
 #endif
@@ -131,7 +159,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CW);
+      mbar_init(&empty[s], RD_EMPTY_COUNT(CW));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -246,14 +274,10 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
           }
         }
       }
-      // release the stage: this warp's reads of the ring (and of the stage
+      // release the stage: this thread's reads of the ring (and of the stage
       // metadata) are ordered before the producer's next cp.async.bulk write
-      // into it by the warp barrier + mbarrier release (RD_RELEASE_FENCE)
-      __syncwarp();
-      if (ln == 0) {
-        RD_RELEASE_FENCE();
-        mbar_arrive(&empty[stage]);
-      }
+      // into it by its mbarrier arrive (release; RD_RELEASE_FENCE)
+      RD_RELEASE_STAGE(&empty[stage]);
       ++cstage;
       if (last) {
         // the chunk's partial: fixed tree over (thread, lane) -> independent of the schedule
@@ -288,15 +312,14 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   __syncthreads();
   __shared__ unsigned s_last;
   if (threadIdx.x == 0) {
-    __threadfence();                                   // release this CTA's chunk partials
-    const unsigned tk = atomicAdd(args.ticket, 1u);
+    // release this CTA's chunk partials (all stored by this thread), acquire the others'
+    const unsigned tk = ticket_acq_rel(args.ticket);
     s_last = (tk == gridDim.x - 1);
     RD_TL(4);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
-  Acc b = fold_slots<OpT, B>(args.partials, args.nchunks);
+  Acc b = fold_slots<OpT, B, 16>(args.partials, args.nchunks);
   if (threadIdx.x == 0) RD_TL(5);
   if (threadIdx.x < args.head) b = fold_at<OpT>(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)), threadIdx.x);
   if (threadIdx.x < args.tail)

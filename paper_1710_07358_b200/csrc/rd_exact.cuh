@@ -827,13 +827,11 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long l
   // a6: last CTA adds the G slots
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned t = atomicAdd(args.ticket, 1u);
+    const unsigned t = ticket_acq_rel(args.ticket);   // release the CTA's slot words, acquire the others'
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   const int G = (int)gridDim.x;
   constexpr int GROUPS = B / (NW + 1);             // (word, slot-group) pairs in parallel
   if (threadIdx.x < GROUPS * (NW + 1)) {
@@ -1040,7 +1038,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
     s_flags = 0;
     for (int st = 0; st < STAGES; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], CW);
+      mbar_init(&empty[st], RD_EMPTY_COUNT(CW));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1138,11 +1136,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
         }
       }
       // reconverge (a replayed vector diverges), then release the stage
-      __syncwarp();
-      if (ln == 0) {
-        RD_RELEASE_FENCE();
-        mbar_arrive(&empty[stage]);
-      }
+      RD_RELEASE_STAGE(&empty[stage]);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
     // a2: head and tail stragglers (< 16 bytes each), CTA 0's first threads

@@ -65,14 +65,3 @@ CombineFn lookup_combine(int dtype, int op) {
 
 }  // namespace rd
 
-#ifdef RD_TIMELINE
-// measurement builds only: the bulk kernel's per-CTA %globaltimer stamps
-extern "C" int rd_timeline_read(void* host, int nctas) {
-  if (nctas > rd::kMaxGrid) nctas = rd::kMaxGrid;
-  return (int)cudaMemcpyFromSymbol(host, rd::rd_tl, (size_t)nctas * 8 * sizeof(unsigned long long));
-}
-extern "C" int rd_timeline_clear(void) {
-  static unsigned long long zero[rd::kMaxGrid][8];
-  return (int)cudaMemcpyToSymbol(rd::rd_tl, zero, sizeof(zero));
-}
-#endif

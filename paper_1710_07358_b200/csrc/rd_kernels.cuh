@@ -72,6 +72,9 @@ struct KArgs {
   Mailbox* self;            // this rank's mailbox
   int* err;                 // sticky status (RD_ERR_MISMATCH / RD_ERR_TIMEOUT)
   int nranks, rank;
+#ifdef RD_TIMELINE
+  unsigned long long* tl;   // measurement builds: [kMaxGrid][8] %globaltimer stamps (rd_bulk.cuh)
+#endif
 };
 
 // Programmatic dependent launch: a kernel launched right behind another may be
@@ -305,23 +308,43 @@ __device__ __forceinline__ void finish_warp0(const typename OpT::Acc& a, const K
 }
 
 // Thread t folds slots t, t+B, t+2B, ... in increasing order (a fixed tree);
-// 8 independent loads in flight per thread.
-template <class OpT, int B>
+// NF independent loads in flight per thread (the bulk kernel's last CTA: 16,
+// one L2 round trip for up to 16 * B chunk slots).
+template <class OpT, int B, int NF = 8>
 __device__ __forceinline__ typename OpT::Acc fold_slots(const Slot* slots, uint32_t count) {
   using Acc = typename OpT::Acc;
   Acc b = OpT::identity();
-  for (uint32_t j0 = threadIdx.x; j0 < count; j0 += 8 * B) {
-    ulonglong2 v[8];
+  for (uint32_t j0 = threadIdx.x; j0 < count; j0 += NF * B) {
+    ulonglong2 v[NF];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < NF; ++k) {
       const uint32_t j = j0 + k * B;
       v[k] = (j < count) ? __ldcg(reinterpret_cast<const ulonglong2*>(slots + j)) : make_ulonglong2(0, 0);
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < NF; ++k)
       if (j0 + k * B < count) b = OpT::combine(b, OpT::unpack(Slot{v[k].x, v[k].y}));
   }
   return b;
+}
+
+// a6 ticket, drawn by thread 0 after a CTA barrier: ONE gpu-scope acq_rel
+// atomic. Its release covers every write the CTA made before the barrier
+// (release is cumulative through bar.sync); its acquire, followed by the next
+// barrier, orders the other CTAs' released writes before every thread's
+// later loads -- the fence + atomic + fence of the classic last-block
+// pattern in one operation (RD_TICKET_FENCES restores that form for A/B).
+__device__ __forceinline__ unsigned ticket_acq_rel(unsigned* p) {
+#ifdef RD_TICKET_FENCES
+  __threadfence();
+  const unsigned r = atomicAdd(p, 1u);
+  __threadfence();
+  return r;
+#else
+  unsigned r;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(r) : "l"(p) : "memory");
+  return r;
+#endif
 }
 
 // a6: one partial per CTA, the last CTA to arrive folds them in index order.
@@ -337,13 +360,11 @@ __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& a
   if (threadIdx.x == 0) {
     Slot s = OpT::pack(a);
     __stcg(reinterpret_cast<ulonglong2*>(args.partials + blockIdx.x), make_ulonglong2(s.a, s.b));
-    __threadfence();                                   // release the partial
-    unsigned t = atomicAdd(args.ticket, 1u);
+    const unsigned t = ticket_acq_rel(args.ticket);    // release the partial, acquire the others
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();                                     // acquire the other partials
   Acc b = fold_slots<OpT, B>(args.partials, gridDim.x);
   b = block_reduce<OpT, B>(b, smem);
   if (threadIdx.x == 0) *args.ticket = 0u;             // reusable by the next launch

@@ -90,3 +90,28 @@ extern "C" int probe_occupancy(int unroll, int threads) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, f, threads, 0);
   return c;
 }
+
+// Launch-gap instrumentation (tools/timeline.py): one thread writes
+// %globaltimer to buf[idx]; and a kernel that only allocates `smem` bytes of
+// dynamic shared memory (switches the SM's L1/shared carveout).
+__global__ void stamp_kernel(unsigned long long* buf, int idx) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  buf[idx] = t;
+}
+__global__ void smem_hog_kernel(int* sink) {
+  extern __shared__ int sm[];
+  if (threadIdx.x == 1023) sm[0] = 1;
+  if (threadIdx.x == 1024) sink[0] = sm[0];
+}
+
+extern "C" int probe_stamp(void* buf, int idx, void* stream) {
+  stamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((unsigned long long*)buf, idx);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int probe_smem_hog(int smem_bytes, int blocks, void* sink, void* stream) {
+  cudaFuncSetAttribute(smem_hog_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  smem_hog_kernel<<<blocks, 32, smem_bytes, (cudaStream_t)stream>>>((int*)sink);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}

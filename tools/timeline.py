@@ -13,6 +13,9 @@ holds only device time: launch latency + kernel), event, reduce, event. The
 read probe (tools/libprobe.so) is timed the same way on the same tensor.
 
     python tools/timeline.py [--lib PATH] [--log2n 25 26 28] [--reps 10]
+    python tools/timeline.py --exp gaps      # launch gaps: stamp kernels around
+        the launch, with and without a preceding 192 KB-shared-memory kernel
+        (the SM's L1/shared carveout already switched), bulk vs vector vs probe
 """
 import argparse
 import ctypes
@@ -69,12 +72,77 @@ def b2b(fn, reps=20):
     return a.elapsed_time(b) * 1e3 / reps
 
 
+def gaps(L, P, args):
+    """stamp0 (end of the preceding work) -> first CTA entry -> output -> stamp1"""
+    st = torch.cuda.current_stream()
+    out = torch.empty(4, dtype=torch.int64, device="cuda")
+    stamps = torch.zeros(8, dtype=torch.int64, device="cuda")
+    hog_sink = torch.zeros(4, dtype=torch.int32, device="cuda")
+    sink = torch.zeros(1 << 20, dtype=torch.int64, device="cuda")
+    cfg_t = type("cfg", (ctypes.Structure,), {"_fields_": [("variant", ctypes.c_int32), ("vec_bytes", ctypes.c_int32),
+                                                             ("unroll", ctypes.c_int32), ("block", ctypes.c_int32),
+                                                             ("grid", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]})
+    L.rd_reduce_ex.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    P.probe_stamp.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    P.probe_smem_hog.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    for log2n in args.log2n:
+        n = 1 << log2n
+        x = torch.empty(n, dtype=torch.float32, device="cuda")
+        inputs.fill_device(x, "u01")
+        nbytes = 4 * n
+        vec = cfg_t(1, 0, 0, 0, 0)
+        impls = {
+            "bulk": lambda: L.reduce(x.data_ptr(), n, 3, 0, out.data_ptr(), st.cuda_stream),
+            "vector": lambda: L.rd_reduce_ex(x.data_ptr(), n, 3, 0, out.data_ptr(), st.cuda_stream,
+                                             ctypes.byref(vec), None),
+            "probe": lambda: P.probe_read(x.data_ptr(), nbytes, 2, 148 * max(1, P.probe_occupancy(2, 256)) * 4, 256,
+                                          sink.data_ptr(), st.cuda_stream, 0),
+        }
+        for name, fn in impls.items():
+            for hog in (0, 1):
+                for _ in range(3):
+                    fn()
+                evs, pre, post, tot = [], [], [], []
+                for _ in range(args.reps):
+                    flush_l2()
+                    torch.cuda._sleep(120_000)
+                    if hog:
+                        P.probe_smem_hog(200 * 1024, 148, hog_sink.data_ptr(), st.cuda_stream)
+                    if name == "bulk":
+                        L.rd_timeline_clear()
+                    P.probe_stamp(stamps.data_ptr(), 0, st.cuda_stream)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(st)
+                    fn()
+                    b.record(st)
+                    P.probe_stamp(stamps.data_ptr(), 1, st.cuda_stream)
+                    torch.cuda.synchronize()
+                    evs.append(a.elapsed_time(b) * 1e3)
+                    s0, s1 = int(stamps[0]), int(stamps[1])
+                    tot.append((s1 - s0) * 1e-3)
+                    if name == "bulk":
+                        tl = (ctypes.c_uint64 * (4096 * 8))()
+                        L.rd_timeline_read(tl, 4096)
+                        ent = [tl[i * 8] for i in range(4096) if tl[i * 8]]
+                        outs = [tl[i * 8 + 7] for i in range(4096) if tl[i * 8 + 7]]
+                        pre.append((min(ent) - s0) * 1e-3)
+                        post.append((s1 - max(outs)) * 1e-3)
+                med = lambda v: round(statistics.median(v), 2) if v else None
+                r = {"exp": "gaps", "log2n": log2n, "impl": name, "after_smem_kernel": bool(hog),
+                     "event_us": med(evs), "stamp_to_stamp_us": med(tot), "stamp0_to_first_entry_us": med(pre),
+                     "output_to_stamp1_us": med(post), "event_gbps": round(nbytes / med(evs) / 1e3, 1)}
+                print(json.dumps(r), flush=True)
+        del x
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--lib", default=os.path.join(ROOT, "build", "ab", "timeline", "libb200reduce.so"))
     ap.add_argument("--log2n", type=int, nargs="*", default=[25, 26, 27, 28])
     ap.add_argument("--pairs", default="float32:sum,int32:sum,float32:argmin")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--exp", default="timeline", choices=["timeline", "gaps"])
     args = ap.parse_args()
     L = ctypes.CDLL(args.lib)
     L.reduce.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
@@ -89,6 +157,8 @@ def main():
     st = torch.cuda.current_stream()
     info = {"device": torch.cuda.get_device_name(), "lib": os.path.relpath(args.lib, ROOT), "reps": args.reps}
     print(json.dumps({"meta": info}), flush=True)
+    if args.exp == "gaps":
+        return gaps(L, P, args)
     for log2n in args.log2n:
         n = 1 << log2n
         for pair in args.pairs.split(","):
@@ -100,6 +170,7 @@ def main():
             for _ in range(5):
                 assert f() == 0
             torch.cuda.synchronize()
+            assert L.rd_timeline_clear() == 0
             ev = cold(f, args.reps)
             # the timeline of the last rep
             tl = (ctypes.c_uint64 * (4096 * 8))()
