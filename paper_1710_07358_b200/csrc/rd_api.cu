@@ -161,9 +161,12 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 // dynamic schedule ends with short chunks and the per-SM tail imbalance is
 // < one C1 chunk. Plain ops: P = 16, Q = 1 (measured best of a sweep,
 // tools/tune_bulk.sh: +0.9% over 12/4/2). Indexed ops (argmin / argmax) pay
-// more per chunk end (the (key, index) tree), so they take fewer, longer tail
-// chunks: P = 4, Q = 4 (tools/ab_lib.py, one box: float32 argmin 6.45 ->
-// 6.82 TB/s, int32 argmax 6.92 -> 7.18, float64 argmin 7.03 -> 7.20).
+// more per chunk end (global indices for the lane bests), so they take fewer,
+// longer tail chunks: P = 4, Q = 4 -- still so after chunk ends became
+// per-thread folds into a running best (rd_bulk.cuh, order-free ops): 4 / 4
+// beat 16 / 1 by 0.9-1.9% on float32 / int32 / uint32 arg ops, float64 even,
+// int64 -0.7% (profiles/ab/r02_ab_cta_partials.jsonl; RD_ARG_TAIL_NARROW
+// builds take 16 / 1).
 struct BulkPlan {
   uint64_t c0, c1, head_region;
   uint32_t nhead, nchunks;
@@ -172,6 +175,9 @@ bool plan_bulk(uint64_t body_bytes, uint64_t stage_bytes, BulkPlan* p, bool inde
   static const uint64_t kHeadPerSm = env_u64("RD_TUNE_HEAD_PER_SM", 16);
   static const uint64_t kTailPerSmEnv = env_u64("RD_TUNE_TAIL_PER_SM", 0);
   static const uint64_t kTailStagesEnv = env_u64("RD_TUNE_TAIL_STAGES", 0);
+#ifdef RD_ARG_TAIL_NARROW
+  indexed = false;
+#endif
   const uint64_t kTailPerSm = kTailPerSmEnv ? kTailPerSmEnv : (indexed ? 4 : 16);
   const uint64_t kTailStages = kTailStagesEnv ? kTailStagesEnv : (indexed ? 4 : 1);
   const uint64_t T = body_bytes;

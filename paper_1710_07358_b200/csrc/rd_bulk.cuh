@@ -9,13 +9,18 @@
 //    a STAGES-deep shared-memory ring with cp.async.bulk (UBLKCP), one
 //    mbarrier per stage carrying the transaction bytes.
 //  consumers: wait on the stage's mbarrier, LDS.128 their fixed slice of the
-//    stage, fold into lane accumulators, release the stage. At the end of a
-//    chunk the CTA reduces the chunk to ONE partial, stored at
-//    partials[chunk] -- so the result does not depend on which CTA took which
-//    chunk: the reduction tree is fixed by n and the base alignment alone
-//    (deterministic, like the vector variant).
-//  last CTA (atomic ticket): folds partials[0..nchunks) in chunk order plus
-//    the head/tail stragglers, writes the result, resets ticket and counter.
+//    stage, fold into lane accumulators, release the stage. Float + and x
+//    (whose bits depend on the evaluation order): at the end of a chunk the
+//    CTA reduces the chunk to ONE partial, stored at partials[chunk] -- so the
+//    result does not depend on which CTA took which chunk: the reduction tree
+//    is fixed by n and the base alignment alone (deterministic, like the
+//    vector variant). Order-free ops (integers, float min/max, arg ops; any
+//    order gives the same result): the lanes run on across chunks (arg ops
+//    fold each chunk's lane bests into a per-thread running best with global
+//    indices), one partial per CTA at the end -- no per-chunk block
+//    reduction, and the last CTA folds gridDim.x slots, not nchunks.
+//  last CTA (atomic ticket): folds the slots in index order plus the
+//    head/tail stragglers, writes the result, resets ticket and counter.
 // In-flight bytes per SM are STAGES * STAGE_BYTES of shared memory (up to
 // 192 KB) instead of registers.
 #pragma once
@@ -143,6 +148,11 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   constexpr int PER_THREAD = STAGE_BYTES / (16 * CT);  // LDS.128 per thread per stage
   static_assert(STAGE_BYTES % (16 * CT) == 0, "stage must split evenly over consumer threads");
   constexpr int B = 32 * (CW + 1);
+#ifdef RD_BULK_CHUNK_PARTIALS
+  constexpr bool kCtaPartial = false;   // (A/B builds) a fixed-tree partial per chunk for every op
+#else
+  constexpr bool kCtaPartial = OrderFree<OpT>::value;
+#endif
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* ring = smem_raw;
@@ -210,6 +220,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
     const int t = threadIdx.x;  // 0 .. CT-1
     using LO = LaneOps<OpT>;
     typename LO::Lane acc[L];
+    Acc run = OpT::identity();   // indexed order-free ops: this thread's best over its finished chunks
 #pragma unroll
     for (int l = 0; l < L; ++l) acc[l] = LO::identity();
     int stage = 0;
@@ -279,7 +290,22 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
       // into it by its mbarrier arrive (release; RD_RELEASE_FENCE)
       RD_RELEASE_STAGE(&empty[stage]);
       ++cstage;
-      if (last) {
+      if (kCtaPartial) {
+        if (last) {
+          if constexpr (OpT::kIndexed) {
+            // the chunk's lane bests with their global indices into the running best
+            uint64_t coff = 0, clen = 0;
+            chunk_range(args, (uint32_t)c, body_bytes, &coff, &clen);
+            const uint64_t e_chunk = args.head + coff / sizeof(T);
+            run = OpT::combine(run, LO::finish(acc, [&](uint32_t st, uint32_t ln) {
+              return e_chunk + ((uint64_t)(st / PER_THREAD) * (STAGE_BYTES / 16) + (st % PER_THREAD) * CT + t) * L + ln;
+            }));
+#pragma unroll
+            for (int l = 0; l < L; ++l) acc[l] = LO::identity();
+          }
+          cstage = 0;
+        }
+      } else if (last) {
         // the chunk's partial: fixed tree over (thread, lane) -> independent of the schedule
         uint64_t coff = 0, clen = 0;
         if constexpr (OpT::kIndexed) chunk_range(args, (uint32_t)c, body_bytes, &coff, &clen);
@@ -306,6 +332,23 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
       }
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
+    if (kCtaPartial) {
+      // order-free ops: the CTA's one partial (identity if it took no chunk)
+      Acc a;
+      if constexpr (OpT::kIndexed) a = run;
+      else a = LO::finish(acc, [](uint32_t, uint32_t) { return (uint64_t)0; });
+      a = OpT::warp_reduce(a);
+      if (ln == 0) wpart[warp] = a;
+      named_sync(1, CT);
+      if (warp == 0) {
+        Acc b = (ln < CW) ? wpart[ln] : OpT::identity();
+        b = OpT::warp_reduce(b);
+        if (ln == 0) {
+          Slot s = OpT::pack(b);
+          __stcg(reinterpret_cast<ulonglong2*>(args.partials + blockIdx.x), make_ulonglong2(s.a, s.b));
+        }
+      }
+    }
   }
   // ------------------------------------------------------------------ grid combine
   pdl_trigger();
@@ -319,7 +362,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   }
   __syncthreads();
   if (!s_last) return;
-  Acc b = fold_slots<OpT, B, 16>(args.partials, args.nchunks);
+  Acc b = fold_slots<OpT, B, 16>(args.partials, kCtaPartial ? gridDim.x : args.nchunks);
   if (threadIdx.x == 0) RD_TL(5);
   if (threadIdx.x < args.head) b = fold_at<OpT>(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)), threadIdx.x);
   if (threadIdx.x < args.tail)

@@ -48,6 +48,7 @@ struct IntOp {
   using Acc = U;
   static constexpr bool kFloat = false;
   static constexpr bool kIndexed = false;
+  static constexpr bool kOrderFree = true;   // mod-2^w ring / lattice ops: any order, same bits
   using S = typename std::conditional<sizeof(U) == 4, int32_t, int64_t>::type;
 
   __device__ __forceinline__ static Acc identity() {
@@ -186,6 +187,7 @@ struct FloatMinMax {
   struct Acc { S key; U amax; };
   static constexpr bool kFloat = true;
   static constexpr bool kIndexed = false;
+  static constexpr bool kOrderFree = true;   // IEEE minimum/maximum on total-order keys
   static constexpr U kAbsMask = (U)(~(U)0) >> 1;
   static constexpr U kInfBits = sizeof(F) == 4 ? (U)0x7f800000u : (U)0x7ff0000000000000ull;
 
@@ -337,6 +339,13 @@ struct FloatSum<double> : Float64SumComp {
   __device__ __forceinline__ static Acc add_block(Acc a, double s) { return two_sum_into(a.hi, a.lo, s); }
 };
 
+// Ops whose result is the same for EVERY evaluation order (not only the same
+// bits for a fixed order): integers, float min/max, argmin/argmax. The bulk
+// kernel folds their chunks into one running partial per CTA instead of one
+// fixed-tree partial per chunk (rd_bulk.cuh).
+template <class O, class = void> struct OrderFree : std::false_type {};
+template <class O> struct OrderFree<O, std::void_t<decltype(O::kOrderFree)>> : std::bool_constant<O::kOrderFree> {};
+
 template <class O, class = void> struct Blocked : std::false_type {};
 template <class O> struct Blocked<O, std::void_t<decltype(O::kBlocked)>> : std::bool_constant<O::kBlocked> {};
 
@@ -376,6 +385,7 @@ struct ArgOp {
   struct Acc { U key; uint64_t idx; };
   static constexpr bool kFloat = (DT == RD_FLOAT32 || DT == RD_FLOAT64);
   static constexpr bool kIndexed = true;
+  static constexpr bool kOrderFree = true;   // lexicographic (key, index): any order, same result
   static constexpr int kBits = 8 * sizeof(U);
   static constexpr U kSign = (U)1 << (kBits - 1);
   static constexpr U kAbs = kSign - 1;
