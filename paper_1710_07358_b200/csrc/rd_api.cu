@@ -355,17 +355,23 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
     uint64_t need = (units + per_cta - 1) / per_cta;
     if (need < 1) need = 1;
     if (g > need) g = need;
-    // Mid sizes (the vector kernel runs below kBulkMinBytes): per-CTA costs
-    // (partial, ticket, the last CTA's fold) outweigh more resident CTAs --
-    // from 12 MiB, 1 CTA/SM up to 48 MiB and 2 above (tools/sweep.py midops,
-    // graph-captured, 7 (dtype, op): 7-16% faster at 16-64 MB; below 12 MiB
-    // the cap cost up to 12%, so it does not apply there).
+    // Mid sizes (the vector kernel runs below kBulkMinBytes): at 12-48 MiB the
+    // grid is capped at 2 CTAs/SM; from 48 MiB it is the occupancy grid.
+    // Measured per (dtype, op) and grid, cold (L2 read-flushed) and L2-warm
+    // (graph-captured), tools/timeline.py --exp grids, profiles/
+    // r02_midsizes_grids.jsonl: float32 sum 2^23 6.2 -> 5.05 us warm, 14.1 ->
+    // 12.3 us cold against round 1's 1 CTA/SM (12-48 MiB) / 2 (48-128 MiB)
+    // cap, argmin 2^24 10.4 -> 8.9 us warm (round 1's graph-captured sweep
+    // had favoured the tighter cap; this build and box do not reproduce it).
+    // Below 12 MiB the work (units / per-CTA) limits the grid anyway.
     // RD_TUNE_VEC_CTAS_PER_SM (RD_TUNING builds only): 0 / unset = this rule,
     // k = k CTAs per SM from 12 MiB, kNoCap = the uncapped occupancy grid.
     constexpr uint64_t kNoCap = 1000;
     static const uint64_t kMidCap = env_u64("RD_TUNE_VEC_CTAS_PER_SM", 0);
-    if (k.variant == RD_VARIANT_VECTOR && kMidCap != kNoCap && (uint64_t)n * s >= (12ull << 20)) {
-      const uint64_t per_sm = kMidCap ? kMidCap : ((uint64_t)n * s >= (48ull << 20) ? 2 : 1);
+    const uint64_t bytes_in = (uint64_t)n * s;
+    if (k.variant == RD_VARIANT_VECTOR && kMidCap != kNoCap && bytes_in >= (12ull << 20) &&
+        (kMidCap || bytes_in < (48ull << 20))) {
+      const uint64_t per_sm = kMidCap ? kMidCap : 2;
       const uint64_t cap = (uint64_t)di.sms * per_sm;
       if (g > cap) g = cap;
     }

@@ -99,8 +99,8 @@ def test_bulk_variant_all_pairs(rd, dtype, op):
 
 def test_auto_planner_choice(rd):
     """The AUTO plan: one CTA up to 32 KB, one cluster of <= 16 CTAs
-    up to 1 MiB, the vector grid (capped at 1 CTA/SM from 12 MiB, 2 from 48 MiB) below
-    128 MiB, the bulk ring from 128 MiB."""
+    up to 1 MiB, the vector grid (capped at 2 CTAs/SM from 12 MiB, the occupancy grid from
+    48 MiB) below 128 MiB, the bulk ring from 128 MiB."""
     sms = torch.cuda.get_device_properties(0).multi_processor_count
 
     def plan(nbytes):
@@ -115,9 +115,9 @@ def test_auto_planner_choice(rd):
     assert p["variant"] == "cluster" and p["grid"] == 16
     assert plan(4 << 20)["variant"] == "vector"
     p = plan(16 << 20)
-    assert p["variant"] == "vector" and p["grid"] == sms
-    p = plan(64 << 20)
     assert p["variant"] == "vector" and p["grid"] == 2 * sms
+    p = plan(64 << 20)
+    assert p["variant"] == "vector" and p["grid"] == sms * p["ctas_per_sm"] and p["ctas_per_sm"] >= 2
     assert plan(128 << 20)["variant"] == "bulk"
     small = to_dev(inputs.generate(1 << 20, "float32", "u01"))
     assert rd.reduce_ex(small, "sum")[1]["variant"] == "vector"

@@ -31,7 +31,8 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 
 DT = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
-OPS = {"sum": 0, "max": 3, "argmin": 7, "argmax": 8, "sum_exact": 10}
+OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "and": 4, "or": 5, "xor": 6, "argmin": 7, "argmax": 8,
+       "sum_compensated": 9, "sum_exact": 10}
 TORCH_DT = {"int32": torch.int32, "float32": torch.float32, "float64": torch.float64, "int64": torch.int64}
 
 _flush = None
@@ -93,7 +94,7 @@ def gaps(L, P, args):
         nbytes = 4 * n
         vec = cfg_t(1, 0, 0, 0, 0)
         impls = {
-            "bulk": lambda: L.reduce(x.data_ptr(), n, 3, 0, out.data_ptr(), st.cuda_stream),
+            "auto": lambda: L.reduce(x.data_ptr(), n, 3, 0, out.data_ptr(), st.cuda_stream),
             "vector": lambda: L.rd_reduce_ex(x.data_ptr(), n, 3, 0, out.data_ptr(), st.cuda_stream,
                                              ctypes.byref(vec), None),
             "probe": lambda: P.probe_read(x.data_ptr(), nbytes, 2, 148 * max(1, P.probe_occupancy(2, 256)) * 4, 256,
@@ -109,7 +110,7 @@ def gaps(L, P, args):
                     torch.cuda._sleep(120_000)
                     if hog:
                         P.probe_smem_hog(200 * 1024, 148, hog_sink.data_ptr(), st.cuda_stream)
-                    if name == "bulk":
+                    if name == "auto":
                         L.rd_timeline_clear()
                     P.probe_stamp(stamps.data_ptr(), 0, st.cuda_stream)
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -121,18 +122,98 @@ def gaps(L, P, args):
                     evs.append(a.elapsed_time(b) * 1e3)
                     s0, s1 = int(stamps[0]), int(stamps[1])
                     tot.append((s1 - s0) * 1e-3)
-                    if name == "bulk":
+                    if name == "auto":
                         tl = (ctypes.c_uint64 * (4096 * 8))()
                         L.rd_timeline_read(tl, 4096)
                         ent = [tl[i * 8] for i in range(4096) if tl[i * 8]]
                         outs = [tl[i * 8 + 7] for i in range(4096) if tl[i * 8 + 7]]
-                        pre.append((min(ent) - s0) * 1e-3)
-                        post.append((s1 - max(outs)) * 1e-3)
+                        if ent and outs:      # AUTO took the bulk kernel (the instrumented one)
+                            pre.append((min(ent) - s0) * 1e-3)
+                            post.append((s1 - max(outs)) * 1e-3)
                 med = lambda v: round(statistics.median(v), 2) if v else None
                 r = {"exp": "gaps", "log2n": log2n, "impl": name, "after_smem_kernel": bool(hog),
                      "event_us": med(evs), "stamp_to_stamp_us": med(tot), "stamp0_to_first_entry_us": med(pre),
                      "output_to_stamp1_us": med(post), "event_gbps": round(nbytes / med(evs) / 1e3, 1)}
                 print(json.dumps(r), flush=True)
+        del x
+
+
+def grids(L, P, args):
+    """mid sizes: the vector kernel's (unroll, grid) -- cold (L2 read-flushed, stamp kernels
+    around the launch: %globaltimer, finer than the events' 2.048 us steps) and L2-warm
+    (100 launches in one CUDA graph) -- next to the bulk kernel and the read probe"""
+    st = torch.cuda.current_stream()
+    out = torch.empty(4, dtype=torch.int64, device="cuda")
+    stamps = torch.zeros(8, dtype=torch.int64, device="cuda")
+    sink = torch.zeros(1 << 20, dtype=torch.int64, device="cuda")
+    cfg_t = type("cfg", (ctypes.Structure,), {"_fields_": [("variant", ctypes.c_int32), ("vec_bytes", ctypes.c_int32),
+                                                             ("unroll", ctypes.c_int32), ("block", ctypes.c_int32),
+                                                             ("grid", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]})
+    L.rd_reduce_ex.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    P.probe_stamp.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    for log2n, pair in [(a, b) for a in args.log2n for b in args.pairs.split(",")]:
+        dtype, op = pair.split(":")
+        dt, opc = DT[dtype], OPS[op]
+        n = 1 << log2n
+        x = torch.empty(n, dtype=TORCH_DT[dtype], device="cuda")
+        inputs.fill_device(x, "u01" if dtype.startswith("float") else "uniform_bits")
+        nbytes = x.element_size() * n
+        cases = {"auto": None, "bulk": cfg_t(3, 0, 0, 0, 0)}
+        for u in (4, 8):
+            for g in (148, 296, 592, 1184):
+                cases[f"vector_u{u}_g{g}"] = cfg_t(1, 32, u, 0, g)
+        for g in (148, 296, 444, 592):      # the default vector kernel (any dtype / op)
+            cases[f"vector_g{g}"] = cfg_t(1, 0, 0, 0, g)
+        for name, cfg in list(cases.items()) + [("probe", "probe")]:
+            cur = lambda: torch.cuda.current_stream().cuda_stream   # the capture stream inside the graph
+            if cfg == "probe":
+                fn = lambda: P.probe_read(x.data_ptr(), nbytes, 2, 148 * max(1, P.probe_occupancy(2, 256)) * 4, 256,
+                                          sink.data_ptr(), cur(), 0)
+            elif cfg is None:
+                fn = lambda: L.reduce(x.data_ptr(), n, dt, opc, out.data_ptr(), cur())
+            else:
+                fn = (lambda c: lambda: L.rd_reduce_ex(x.data_ptr(), n, dt, opc, out.data_ptr(), cur(),
+                                                       ctypes.byref(c), None))(cfg)
+            if fn() != 0 and cfg != "probe":
+                continue
+            if args.cases and name not in args.cases:
+                continue
+            for _ in range(3):
+                fn()
+            tot = []
+            for _ in range(args.reps):
+                flush_l2()
+                torch.cuda._sleep(120_000)
+                P.probe_stamp(stamps.data_ptr(), 0, st.cuda_stream)
+                fn()
+                P.probe_stamp(stamps.data_ptr(), 1, st.cuda_stream)
+                torch.cuda.synchronize()
+                tot.append((int(stamps[1]) - int(stamps[0])) * 1e-3)
+            # L2-warm: 100 launches captured in one graph
+            gs = torch.cuda.Stream()
+            gs.wait_stream(st)
+            with torch.cuda.stream(gs):
+                fn()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(100):
+                    fn()
+            g.replay()
+            torch.cuda.synchronize()
+            ws = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                g.replay()
+                b.record(st)
+                b.synchronize()
+                ws.append(a.elapsed_time(b) * 10.0)
+            r = {"exp": "grids", "dtype": dtype, "op": op, "log2n": log2n, "case": name, "cold_stamp_us": round(statistics.median(tot), 2),
+                 "cold_stamp_min_us": round(min(tot), 2), "warm_graph_us": round(statistics.median(ws), 2)}
+            print(json.dumps(r), flush=True)
+            del g
         del x
 
 
@@ -142,12 +223,14 @@ def main():
     ap.add_argument("--log2n", type=int, nargs="*", default=[25, 26, 27, 28])
     ap.add_argument("--pairs", default="float32:sum,int32:sum,float32:argmin")
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--exp", default="timeline", choices=["timeline", "gaps"])
+    ap.add_argument("--exp", default="timeline", choices=["timeline", "gaps", "grids"])
+    ap.add_argument("--cases", nargs="*", default=None, help="grids: only these cases")
     args = ap.parse_args()
     L = ctypes.CDLL(args.lib)
     L.reduce.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                          ctypes.c_void_p]
-    L.rd_timeline_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    if hasattr(L, "rd_timeline_read"):      # RD_TIMELINE builds only
+        L.rd_timeline_read.argtypes = [ctypes.c_void_p, ctypes.c_int]
     P = ctypes.CDLL(os.path.join(ROOT, "tools", "libprobe.so"))
     P.probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
@@ -159,6 +242,8 @@ def main():
     print(json.dumps({"meta": info}), flush=True)
     if args.exp == "gaps":
         return gaps(L, P, args)
+    if args.exp == "grids":
+        return grids(L, P, args)
     for log2n in args.log2n:
         n = 1 << log2n
         for pair in args.pairs.split(","):
