@@ -98,11 +98,11 @@ def _check_out(out, dtype, op):
 
 
 def _arg_view(buf, dtype):
-    """rd_arg_result buffer (2 x int64) -> (value 0-d tensor of dtype, index 0-d int64)."""
-    torch = _torch()
-    esz = torch.empty((), dtype=dtype).element_size()
-    value = buf[0:1].view(torch.uint8)[:esz].view(dtype)[0]
-    return value, buf[1]
+    """rd_arg_result buffer (2 x int64) -> (value 0-d tensor of dtype, index 0-d int64).
+    The value's bits are the low sizeof(dtype) bytes of word 0 (little endian), i.e.
+    element 0 of the buffer viewed as dtype (two view ops: ~5 us of host time per
+    call instead of ~21 us for a byte-slicing view chain)."""
+    return buf.view(dtype)[0], buf[1]
 
 
 def _result(out, dtype, op):

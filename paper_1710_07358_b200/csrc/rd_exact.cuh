@@ -473,46 +473,93 @@ __device__ __noinline__ ExState<E, GL> exact64_elementwise(ExState<E, GL> st, co
   return st;
 }
 
-// fp64 data, a GROUP of GL elements into one expansion (a0, a1), speculating
-// on facts one integer bookkeeping pass per group proves:
-//  * Fast2Sum is exact: every running a0 has an exponent >= every x's
-//    (min |a0| hi word >= max |x| hi word), so a0 + x = s + e with
-//    e = x - (s - a0): 3 DADD instead of TwoSum's 6;
-//  * the GL errors sum exactly in a tree: each e is a multiple of ulp(x) >=
-//    2^(xmin - 1075) (a0 is a multiple of it too; if s lands below x's
-//    binade the add was exact, e = 0) and |e| <= ulp(s)/2 <= 2^(smax - 1076),
-//    so with smax - xmin <= 54 - log2(GL) every partial fits 53 bits;
-//  * ONE tested add puts the error sum into a1 (as spec2's test).
-// 3 + 7/8 + 5/8 FP64 ops per element instead of spec2's 11, plus 6 integer
-// ops (|hi|, max, min(|hi| - 1) for x; |hi|, min, max for a0). Overflow,
-// inf/NaN, a small running sum (|a0| below some |x|: every thread's first
-// group, sign changes of the sum), wide groups or an inexact a1 add: the
-// per-element levels, out of line.
+// fp64 data, a GROUP of GL elements into one expansion (a0, a1): the GL
+// errors of the adds into a0 are summed in a tree and ONE tested add puts that
+// sum into a1 (as spec2's test). The error tree is exact when every error is
+// a multiple of 2^m (m: the smallest ulp among the terms and the running sums
+// they meet) and below half an ulp of the largest running sum: the exponent
+// spread <= 54 - log2(GL) -- or trivially when every error is 0 (e.g. terms
+// on a common grid, such as the normalish workload's multiples of 2^-24).
+// Two forms, chosen per warp BEFORE the group work from facts the terms and
+// the current a0 give:
+//  * Fast2Sum (3 DADD per element instead of TwoSum's 6) when every lane's
+//    |a0| >= GL * max |x| (exponent of a0 >= that of max |x| + 1 + log2 GL):
+//    then every running sum outweighs every term, so a0 + x = s + e with
+//    e = x - (s - a0) exactly. 3 + 7/8 + 5/8 FP64 ops per element (spec2:
+//    11). Same-sign data (u01) lives here after its first groups.
+//  * TwoSum otherwise (zero-mean data whose running sums cross zero, every
+//    thread's first groups): 6 + 7/8 + 5/8 -- still below spec2's 11, with no
+//    wasted speculation. (Speculating Fast2Sum and replaying on failure had
+//    cost zero-mean fp64 data 15-29%: with 32 lanes per warp some lane's sum
+//    is nearly always near zero.)
+// inf/NaN terms or a spread of the terms alone past the bound: the
+// per-element levels straight away; an overflow, a spread past the bound
+// (with the running sums) with a nonzero error, or an inexact a1 add: the
+// group is replayed through them. Both out of line.
 template <int E, int GL>
 __device__ __forceinline__ void fold_group_exact64(Ex (&ex)[E], int g, const double (&x)[GL], long long* w,
                                                    uint32_t& flags) {
   static_assert(GL == 4 || GL == 8, "group of 4 or 8 doubles");
-  constexpr int kMaxSpread = 54 - (GL == 4 ? 2 : 3);
+  constexpr int kLog2GL = (GL == 4 ? 2 : 3);
+  constexpr int kMaxSpread = 54 - kLog2GL;
+  const unsigned mask = __activemask();
   Ex& q = ex[g % E];
-  uint32_t xmax = 0, xmin = 0xffffffffu, amin = 0xffffffffu, smax = 0;
-  double a = q.a0, e[GL];
+  uint32_t xmax = 0, xmin = 0xffffffffu;
 #pragma unroll
   for (int l = 0; l < GL; ++l) {
     const uint32_t xh = (uint32_t)__double2hiint(x[l]) & 0x7fffffffu;
     xmax = max(xmax, xh);
     xmin = min(xmin, xh - 1u);                       // zero -> 0xffffffff: no effect
-    amin = min(amin, (uint32_t)__double2hiint(a) & 0x7fffffffu);
-    const double sl = __dadd_rn(a, x[l]);
-    e[l] = __dsub_rn(x[l], __dsub_rn(sl, a));        // Fast2Sum
-    a = sl;
-    smax = max(smax, (uint32_t)__double2hiint(a) & 0x7fffffffu);
   }
+  // inf/NaN terms, or terms too far apart for any exact error tree: the
+  // per-element levels straight away (no group work to throw away)
+  if (__builtin_expect(__any_sync(mask, (xmax >= 0x7ff00000u) |
+                                            ((int)(xmax >> 20) - (int)(xmin >> 20) > kMaxSpread)), 0)) {
+    ExState<E, GL> st;
+#pragma unroll
+    for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
+    st.flags = flags;
+    ExVals<GL> v;
+#pragma unroll
+    for (int l = 0; l < GL; ++l) v.v[l] = x[l];
+    st = exact64_elementwise<E, GL>(st, v, w);
+#pragma unroll
+    for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
+    flags = st.flags;
+    return;
+  }
+  const uint32_t a0h = (uint32_t)__double2hiint(q.a0) & 0x7fffffffu;
+  const bool fast = __all_sync(mask, (a0h >> 20) >= (xmax >> 20) + 1 + kLog2GL);
+  double a = q.a0, e[GL];
+  uint32_t smax = 0, amin = 0xffffffffu;
+  if (fast) {
+#pragma unroll
+    for (int l = 0; l < GL; ++l) {
+      const double sl = __dadd_rn(a, x[l]);
+      e[l] = __dsub_rn(x[l], __dsub_rn(sl, a));      // Fast2Sum: |a| >= |x| here
+      a = sl;
+      smax = max(smax, (uint32_t)__double2hiint(a) & 0x7fffffffu);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < GL; ++l) {
+      amin = min(amin, ((uint32_t)__double2hiint(a) & 0x7fffffffu) - 1u);   // zero sums drop out
+      double sl;
+      two_sum(a, x[l], sl, e[l]);
+      a = sl;
+      smax = max(smax, (uint32_t)__double2hiint(a) & 0x7fffffffu);
+    }
+  }
+  bool nz = false;
+#pragma unroll
+  for (int l = 0; l < GL; ++l) nz |= (e[l] != 0.0);
+  const uint32_t mn = min(xmin, amin);
   const double se = tree_sum<GL>(e);
   const double t = __dadd_rn(q.a1, se);
-  const bool bad = (smax >= 0x7ff00000u) | (xmax >= 0x7ff00000u) | (amin < xmax) |
-                   ((int)(smax >> 20) - (int)(xmin >> 20) > kMaxSpread) |
+  const bool bad = (smax >= 0x7ff00000u) | (xmax >= 0x7ff00000u) |
+                   (nz & ((int)(smax >> 20) - (int)(mn >> 20) > kMaxSpread)) |
                    (__dsub_rn(t, q.a1) != se) | (__dsub_rn(t, se) != q.a1);
-  if (__builtin_expect(!__any_sync(__activemask(), bad), 1)) {
+  if (__builtin_expect(!__any_sync(mask, bad), 1)) {
     q.a0 = a;
     q.a1 = t;
     return;

@@ -19,6 +19,7 @@ PAIRS = [("float32", "argmin"), ("float32", "argmax"), ("int32", "argmax"), ("fl
          ("float32", "sum"), ("int32", "sum"), ("float64", "max"), ("int64", "argmin"), ("uint32", "argmax")]
 if os.environ.get("AB_PAIRS"):            # e.g. AB_PAIRS=uint32:argmax,float32:argmin
     PAIRS = [tuple(p.split(":")) for p in os.environ["AB_PAIRS"].split(",")]
+# AB_WORKLOAD: the float workload (default u01; e.g. normalish, wide)
 # AB_SOAK=S: S seconds of back-to-back calls before each timing (the sustained,
 # power-capped regime bench.py measures); AB_REPS: calls per timing
 SOAK = float(os.environ.get("AB_SOAK", "0"))
@@ -97,7 +98,7 @@ if __name__ == "__main__":
     xs = {}
     for dtype in ("float32", "int32", "float64", "int64", "uint32"):
         xs[dtype] = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
-        inputs.fill_device(xs[dtype], "u01" if dtype.startswith("float") else "int_small", seed=1)
+        inputs.fill_device(xs[dtype], os.environ.get("AB_WORKLOAD", "u01") if dtype.startswith("float") else "int_small", seed=1)
     for rnd in range(2):                      # interleaved twice: clock drift shows up
         for p in sys.argv[1:]:
             print(json.dumps({"lib": os.path.basename(p), "round": rnd, **run(p, xs)}), flush=True)
