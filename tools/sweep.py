@@ -423,10 +423,75 @@ def do_overhead(args):
     return rows
 
 
+def do_context(args):
+    """SURVEY §8(d) context rows on the same box, across sizes: this library vs CUB
+    DeviceReduce::Reduce (tools/libcubref.so) vs torch.sum / torch.amax vs the read
+    probe, float32 / int32 sum and max. Per launch: graph-captured back to back (100
+    launches in one CUDA graph; L2-warm below ~L2 size) and cold (L2 read-flushed,
+    a device spin, %globaltimer stamp kernels around the launch; kernel boundaries
+    land on ~2.05 us steps, so medians move in those steps)."""
+    cub = ctypes.CDLL(os.path.join(ROOT, "tools", "libcubref.so"))
+    cub.cub_ref_reduce.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                   ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t), ctypes.c_void_p]
+    pl = ctypes.CDLL(os.path.join(ROOT, "tools", "libprobe.so"))
+    pl.probe_read.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+    pl.probe_stamp.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    sink = torch.zeros(1 << 20, dtype=torch.int32, device="cuda")
+    stamps = torch.zeros(4, dtype=torch.int64, device="cuda")
+    cur = lambda: torch.cuda.current_stream().cuda_stream
+    rows = []
+    sizes = args.log2n if args.log2n != [28] else list(range(16, 31, 2))
+    for dtype in ("float32", "int32"):
+        for op in ("sum", "max"):
+            for log2n in sizes:
+                n = 1 << log2n
+                x = make(n, dtype, "u01" if dtype == "float32" else "uniform_bits")
+                nbytes = 4 * n
+                o = torch.empty((), dtype=x.dtype, device="cuda")
+                ot = torch.empty((), dtype=torch.int64 if (dtype == "int32" and op == "sum") else x.dtype,
+                                 device="cuda")
+                co = torch.empty(2, dtype=torch.int64, device="cuda")
+                code_dt, code_op = (3 if dtype == "float32" else 0), (0 if op == "sum" else 3)
+                nb = ctypes.c_size_t(0)
+                assert cub.cub_ref_reduce(x.data_ptr(), n, code_dt, code_op, co.data_ptr(), None, ctypes.byref(nb),
+                                          cur()) == 0
+                tmp = torch.empty(max(1, nb.value), dtype=torch.uint8, device="cuda")
+                blocks = 148 * max(1, pl.probe_occupancy(2, 256)) * 4
+                impls = {
+                    "b200reduce": lambda: rd.reduce(x, op, out=o),
+                    "cub": lambda: cub.cub_ref_reduce(x.data_ptr(), n, code_dt, code_op, co.data_ptr(),
+                                                      tmp.data_ptr(), ctypes.byref(nb), cur()),
+                    "torch": ((lambda: torch.sum(x, dim=0, dtype=ot.dtype, out=ot)) if op == "sum"
+                              else (lambda: torch.amax(x, dim=0, out=ot))),
+                    "read_probe": lambda: pl.probe_read(x.data_ptr(), nbytes, 2, blocks, 256, sink.data_ptr(),
+                                                        cur(), 0),
+                }
+                for name, fn in impls.items():
+                    g = graph_us(fn)
+                    cold = []
+                    for _ in range(7):
+                        flush_l2()
+                        torch.cuda._sleep(100_000)
+                        pl.probe_stamp(stamps.data_ptr(), 0, cur())
+                        fn()
+                        pl.probe_stamp(stamps.data_ptr(), 1, cur())
+                        torch.cuda.synchronize()
+                        cold.append((int(stamps[1]) - int(stamps[0])) * 1e-3)
+                    c = statistics.median(cold)
+                    r = {"dtype": dtype, "op": op, "log2n": log2n, "impl": name, "graph_us": round(g, 3),
+                         "graph_gbps": round(nbytes / g / 1e3, 1), "cold_us": round(c, 2),
+                         "cold_gbps": round(nbytes / c / 1e3, 1)}
+                    rows.append(r)
+                    print(json.dumps(r), flush=True)
+                del x, tmp
+    return rows
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi", "overhead",
-                                    "exact", "midgrids", "midops"])
+                                    "exact", "midgrids", "midops", "context"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
@@ -434,7 +499,7 @@ def main():
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
            "grids": do_grids, "crossover": do_crossover, "multi": do_multi,
            "overhead": do_overhead, "exact": do_exact,
-           "midgrids": do_midgrids, "midops": do_midops}[args.what](args)
+           "midgrids": do_midgrids, "midops": do_midops, "context": do_context}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
         json.dump({"meta": meta, "result": res}, f, indent=1)
