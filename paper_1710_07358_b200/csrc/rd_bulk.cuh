@@ -119,20 +119,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
-// RD_TIMELINE (measurement builds only, tools/timeline.py): %globaltimer
-// stamps per CTA -- entry, first full stage, stream end, ticket, and the last
-// CTA's fold / block reduce / output -- read back with rd_timeline_read (rd_api.cu).
-#ifdef RD_TIMELINE
-__device__ __forceinline__ unsigned long long rd_gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define RD_TL(slot) (args.tl[blockIdx.x * 8 + (slot)] = rd_gtimer())
-#else
-#define RD_TL(slot) ((void)0)
-#endif
-
 template <int STAGES, int STAGE_BYTES, int CW>
 struct BulkSmem {
   static constexpr int kRing = STAGES * STAGE_BYTES;

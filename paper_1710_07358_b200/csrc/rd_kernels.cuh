@@ -85,6 +85,21 @@ struct KArgs {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// RD_TIMELINE (measurement builds only, tools/timeline.py): %globaltimer
+// stamps per CTA -- 0 entry, 1 first full stage (bulk), 2 stream end, 3 the
+// producer out of chunks (bulk), 4 ticket, and the last CTA's 5 fold / 6 block
+// reduce / 7 output -- read back with rd_timeline_read (rd_api.cu).
+#ifdef RD_TIMELINE
+__device__ __forceinline__ unsigned long long rd_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define RD_TL(slot) (args.tl[blockIdx.x * 8 + (slot)] = rd_gtimer())
+#else
+#define RD_TL(slot) ((void)0)
+#endif
+
 // Thread-block cluster primitives (sm_90+): a full cluster barrier with
 // release/acquire semantics (orders shared-memory writes before the DSMEM
 // reads of other CTAs), the CTA's rank and the cluster size, and a 16-byte
@@ -362,13 +377,19 @@ __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& a
     __stcg(reinterpret_cast<ulonglong2*>(args.partials + blockIdx.x), make_ulonglong2(s.a, s.b));
     const unsigned t = ticket_acq_rel(args.ticket);    // release the partial, acquire the others
     s_last = (t == gridDim.x - 1);
+    RD_TL(4);
   }
   __syncthreads();
   if (!s_last) return;
   Acc b = fold_slots<OpT, B>(args.partials, gridDim.x);
+  if (threadIdx.x == 0) RD_TL(5);
   b = block_reduce<OpT, B>(b, smem);
-  if (threadIdx.x == 0) *args.ticket = 0u;             // reusable by the next launch
+  if (threadIdx.x == 0) {
+    RD_TL(6);
+    *args.ticket = 0u;                                 // reusable by the next launch
+  }
   if (threadIdx.x < 32) finish_warp0<OpT>(b, args);
+  if (threadIdx.x == 0) RD_TL(7);
 }
 
 // ---------------------------------------------------------------- a1-a5
@@ -390,6 +411,7 @@ __device__ __forceinline__ typename OpT::Acc vector_body(const KArgs& args, type
   const uint64_t stride = (uint64_t)gridDim.x * B;
   const unsigned char* body = args.x + args.head * sizeof(T);
   pdl_wait();
+  if (threadIdx.x == 0) RD_TL(0);
   const uint64_t nvec = args.nvec;
   uint64_t i = tid;
   uint32_t step = 0;   // vector slot tid + step*stride (indexed ops only)
@@ -429,6 +451,7 @@ template <class OpT, int B, int U, int VB>
 __global__ void __launch_bounds__(B, 1) rd_vector_kernel(const KArgs args) {
   __shared__ typename OpT::Acc smem[32];
   typename OpT::Acc a = vector_body<OpT, B, U, VB>(args, smem);
+  if (threadIdx.x == 0) RD_TL(2);
   __syncthreads();  // smem is reused by the grid combine
   grid_combine<OpT, B>(a, args, smem);
 }

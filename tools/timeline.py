@@ -45,12 +45,16 @@ def flush_l2():
     _flush.max()
 
 
-def cold(fn, reps):
-    """device time of single launches, host enqueue hidden behind a spin"""
+def cold(fn, reps, warm=False):
+    """device time of single launches, host enqueue hidden behind a spin
+    (warm: no L2 flush -- the previous launch left the input in L2)"""
     s = torch.cuda.current_stream()
     ts = []
     for _ in range(reps):
-        flush_l2()
+        if warm:
+            fn()
+        else:
+            flush_l2()
         torch.cuda._sleep(120_000)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
@@ -160,8 +164,8 @@ def grids(L, P, args):
         inputs.fill_device(x, "u01" if dtype.startswith("float") else "uniform_bits")
         nbytes = x.element_size() * n
         cases = {"auto": None, "bulk": cfg_t(3, 0, 0, 0, 0)}
-        for u in (4, 8):
-            for g in (148, 296, 592, 1184):
+        for u in args.us:
+            for g in args.gs:
                 cases[f"vector_u{u}_g{g}"] = cfg_t(1, 32, u, 0, g)
         for g in (148, 296, 444, 592):      # the default vector kernel (any dtype / op)
             cases[f"vector_g{g}"] = cfg_t(1, 0, 0, 0, g)
@@ -224,7 +228,10 @@ def main():
     ap.add_argument("--pairs", default="float32:sum,int32:sum,float32:argmin")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--exp", default="timeline", choices=["timeline", "gaps", "grids"])
+    ap.add_argument("--warm", action="store_true", help="timeline: no L2 flush (L2-resident inputs)")
     ap.add_argument("--cases", nargs="*", default=None, help="grids: only these cases")
+    ap.add_argument("--us", type=int, nargs="*", default=[4, 8], help="grids: vector unrolls (ablation kernels)")
+    ap.add_argument("--gs", type=int, nargs="*", default=[148, 296, 592, 1184], help="grids: vector grids")
     args = ap.parse_args()
     L = ctypes.CDLL(args.lib)
     L.reduce.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
@@ -256,7 +263,7 @@ def main():
                 assert f() == 0
             torch.cuda.synchronize()
             assert L.rd_timeline_clear() == 0
-            ev = cold(f, args.reps)
+            ev = cold(f, args.reps, args.warm)
             # the timeline of the last rep
             tl = (ctypes.c_uint64 * (4096 * 8))()
             assert L.rd_timeline_read(tl, 4096) == 0
@@ -275,13 +282,13 @@ def main():
                                       sink.data_ptr(), st.cuda_stream, 0)
             for _ in range(3):
                 pf()
-            pev = cold(pf, args.reps)
+            pev = cold(pf, args.reps, args.warm)
             r = {"dtype": dtype, "op": op, "log2n": log2n, "grid": len(rows),
                  "cold_event_us": round(statistics.median(ev), 2), "cold_event_min_us": round(min(ev), 2),
                  "probe_cold_event_us": round(statistics.median(pev), 2),
                  "b2b_us": round(b2b(f), 2), "probe_b2b_us": round(b2b(pf), 2),
                  "span_us": round(rel(last[7]), 2),
-                 "entry_spread_us": round(max(ent), 2),
+                 "entry_spread_us": round(max(ent), 2), "entry_med_us": round(statistics.median(ent), 2),
                  "first_data_us_med": round(statistics.median(first), 2) if first else None,
                  "producer_done_us": [round(pend[0], 2), round(pend[len(pend) // 2], 2), round(pend[-1], 2)] if pend else None,
                  "stream_end_us": [round(send[0], 2), round(send[len(send) // 2], 2), round(send[-1], 2)],
