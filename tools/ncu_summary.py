@@ -2,7 +2,9 @@
 """Summarise ncu captures for profiles/ (run here, on the CPU box).
 
     python tools/ncu_summary.py launches <launches.csv>          # per-kernel launch list
-    python tools/ncu_summary.py full <prof.ncu-rep> [algorithmic_bytes]
+    python tools/ncu_summary.py full <prof.ncu-rep> [algorithmic_bytes | n:<elements>]
+(n:<elements>: algorithmic bytes = n * the element size read off each kernel's
+template arguments -- 8 for double / 64-bit integer kernels, else 4)
 """
 import csv
 import io
@@ -71,10 +73,17 @@ def full(path, alg_bytes=None):
                     stalls[k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", "")] = v
         d["stalls_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1]))
         if alg_bytes:
+            if str(alg_bytes).startswith("n:"):
+                kn = d["kernel"]
+                wide = any(t in kn for t in ("double", "unsigned long", "Float64", "<long"))
+                alg = int(str(alg_bytes)[2:]) * (8 if wide else 4)
+            else:
+                alg = float(alg_bytes)
+            d["algorithmic_bytes"] = alg
             rd = float(vals[h.index("dram__bytes_read.sum")]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[units[h.index("dram__bytes_read.sum")]]
             wr = float(vals[h.index("dram__bytes_write.sum")]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}[units[h.index("dram__bytes_write.sum")]]
             d["traffic_bytes"] = rd + wr
-            d["traffic_over_algorithmic"] = (rd + wr) / float(alg_bytes)
+            d["traffic_over_algorithmic"] = (rd + wr) / float(alg)
         res.append(d)
     return res
 

@@ -14,7 +14,8 @@ import inputs  # noqa: E402
 import paper_1710_07358_b200 as rd  # noqa: E402
 
 PAIRS = [("int32", "sum"), ("float64", "sum"), ("float64", "prod"), ("float32", "max"),
-         ("float32", "argmin"), ("float64", "sum_compensated")]
+         ("float32", "argmin"), ("float64", "sum_compensated"), ("float32", "argmax"), ("float64", "argmin"),
+         ("float64", "max"), ("int64", "xor"), ("float32", "prod")]
 # `python tools/profile_ops.py exact`: the exact sum on its two data classes
 EXACT = [("float32", "sum_exact"), ("float64", "sum_exact")]
 
