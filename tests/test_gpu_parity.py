@@ -852,6 +852,38 @@ def test_c5_full_size_2_34(rd):
     del x
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype", ["float32", "int64"])
+def test_indices_past_2_32_every_variant(rd, dtype):
+    """Element indices >= 2^32 through each variant's own index arithmetic (vector:
+    head + (tid + step*stride)*L + lane; bulk: chunk offset + stage step; cluster
+    and forced small grids make the per-thread step counts large): n = 2^32 + 12345
+    'planted' data with the extremes moved past 2^32, a TIE for the minimum (the
+    lower index must win) and an odd base offset; argmax / argmin / max / min
+    against these closed forms, every variant and two grids."""
+    s = 4 if dtype == "float32" else 8
+    free, _ = torch.cuda.mem_get_info()
+    if free < ((1 << 32) + 20000) * s + (8 << 30):
+        pytest.skip("needs ~%d GiB of free HBM" % (((1 << 32) * s >> 30) + 8))
+    n = (1 << 32) + 12345
+    buf = torch.empty(n + 1, dtype=getattr(torch, dtype), device="cuda")
+    x = buf[1:]                                    # element-aligned, not vector-aligned
+    inputs.fill_device(x, "planted", seed=2)
+    hi, lo = (2.0 ** 21, -2.0 ** 21) if dtype == "float32" else (1 << 40, -5)
+    i_max, i_min, i_min2 = (1 << 32) + 777, (1 << 32) + 999, (1 << 32) + 5000
+    x[i_max] = hi
+    x[i_min] = lo
+    x[i_min2] = lo                                 # tie: the lower index wins
+    npdt = np.float32 if dtype == "float32" else np.int64
+    for variant, grid in (("auto", 0), ("vector", 0), ("vector", 37), ("bulk", 0), ("bulk", 5), ("cluster", 16)):
+        got = {op: val(rd.reduce_ex(x, op, variant=variant, grid=grid)[0])
+               for op in ("argmax", "argmin", "max", "min")}
+        assert got["argmax"] == (npdt(hi), i_max), (variant, grid, got["argmax"])
+        assert got["argmin"] == (npdt(lo), i_min), (variant, grid, got["argmin"])
+        assert got["max"] == npdt(hi) and got["min"] == npdt(lo), (variant, grid, got)
+    del buf, x
+
+
 def test_c_program_through_the_abi(rd, tmp_path):
     """A plain C99 program (examples/reduce_example.c) drives the library: exact
     sum of ones, argmax tie -> index 0, and back-to-back reduce() calls."""
