@@ -408,12 +408,30 @@ __device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L
   }
 }
 
+// The per-element levels for a group whose group speculation failed, in
+// pieces of P elements: each piece speculates (fold_vec_exact) and replays on
+// its own, so one inexact element replays P elements, not the whole group --
+// on data whose adds are mostly inexact (the `wide` workload) the replay
+// probability grows with the piece size (round 1 speculated per LDS.128
+// vector: 4 floats / 2 doubles; whole groups of 8 had cost `wide` 25% / 11%).
+template <typename T, int E, int GL, int P>
+__device__ __forceinline__ void elementwise_pieces(ExState<E, GL>& st, const ExVals<GL>& xs, long long* w) {
+#pragma unroll
+  for (int p = 0; p < GL; p += P) {
+    double piece[P];
+#pragma unroll
+    for (int l = 0; l < P; ++l) piece[l] = xs.v[p + l];
+    fold_vec_exact<T, E, P>(st.ex, piece, w, st.flags);
+  }
+}
+
 // fp32 data, the per-element path for one group whose group speculation
 // failed, out of line (one copy per kernel): fold_vec_exact's levels --
-// tested adds into a0, then two TwoSum levels, then the element replay.
+// tested adds into a0, then two TwoSum levels, then the element replay --
+// per 4 elements.
 template <int E, int GL>
 __device__ __noinline__ ExState<E, GL> exact32_elementwise(ExState<E, GL> st, const ExVals<GL> xs, long long* w) {
-  fold_vec_exact<float, E, GL>(st.ex, xs.v, w, st.flags);
+  elementwise_pieces<float, E, GL, (GL < 4 ? GL : 4)>(st, xs, w);
   return st;
 }
 
@@ -466,10 +484,10 @@ __device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], int g, const uin
   flags = st.flags;
 }
 
-// fp64 data, the per-element path for one group (out of line)
+// fp64 data, the per-element path for one group (out of line), per 2 elements
 template <int E, int GL>
 __device__ __noinline__ ExState<E, GL> exact64_elementwise(ExState<E, GL> st, const ExVals<GL> xs, long long* w) {
-  fold_vec_exact<double, E, GL>(st.ex, xs.v, w, st.flags);
+  elementwise_pieces<double, E, GL, 2>(st, xs, w);
   return st;
 }
 
