@@ -163,6 +163,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
 
   const unsigned char* body = args.x + args.head * sizeof(T);
   const uint64_t body_bytes = args.nvec * 16;
+  constexpr bool kPacked = RD_PACKED_SUM && PackedSum32<OpT>::value;
+  Acc cta_part = OpT::identity();   // kPacked: the CTA's partial, in thread 0
   pdl_wait();
   if (threadIdx.x == 0) RD_TL(0);
 
@@ -330,8 +332,12 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
         Acc b = (ln < CW) ? wpart[ln] : OpT::identity();
         b = OpT::warp_reduce(b);
         if (ln == 0) {
-          Slot s = OpT::pack(b);
-          __stcg(reinterpret_cast<ulonglong2*>(args.partials + blockIdx.x), make_ulonglong2(s.a, s.b));
+          if constexpr (kPacked) {
+            cta_part = b;
+          } else {
+            Slot s = OpT::pack(b);
+            __stcg(reinterpret_cast<ulonglong2*>(args.partials + blockIdx.x), make_ulonglong2(s.a, s.b));
+          }
         }
       }
     }
@@ -339,6 +345,31 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_bulk_kernel(const KArgs a
   // ------------------------------------------------------------------ grid combine
   pdl_trigger();
   __syncthreads();
+  if constexpr (kPacked) {
+    // 32-bit integer +: the total from the arrival atomic itself (no slots)
+    __shared__ unsigned s_done;
+    __shared__ uint32_t s_total;
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      s_done = packed_arrive<true>(args.ticket, cta_part, &tot);
+      s_total = tot;
+      if (s_done) *args.work = 0u;
+      RD_TL(4);
+    }
+    __syncthreads();
+    if (!s_done) return;
+    if (threadIdx.x < 32) {   // warp 0: the total + the head / tail stragglers (< 4 each)
+      Acc b = threadIdx.x == 0 ? (Acc)s_total : OpT::identity();
+      if (threadIdx.x < args.head) b = fold_at<OpT>(b, ldg_scalar<T>(args.x + threadIdx.x * sizeof(T)), threadIdx.x);
+      if (threadIdx.x < args.tail)
+        b = fold_at<OpT>(b, ldg_scalar<T>(args.x + (args.tail_start + threadIdx.x) * sizeof(T)),
+                         args.tail_start + threadIdx.x);
+      b = OpT::warp_reduce(b);
+      finish_warp0<OpT>(b, args);
+    }
+    if (threadIdx.x == 0) RD_TL(7);
+    return;
+  }
   __shared__ unsigned s_last;
   if (threadIdx.x == 0) {
     // release this CTA's chunk partials (all stored by this thread), acquire the others'

@@ -362,6 +362,32 @@ __device__ __forceinline__ unsigned ticket_acq_rel(unsigned* p) {
 #endif
 }
 
+// a6 for 32-bit integer + (PackedSum32): thread 0 adds {a << 32 | 1} to the
+// 64-bit word at the ticket. The vector kernels read no other CTA's memory --
+// the total arrives in the atomic's return value -- so relaxed suffices (the
+// reset is ordered after every add by the word's own coherence order); the
+// bulk kernel (ACQ_REL) also orders every producer's chunk-counter atomics
+// before the last CTA resets that counter. Returns true in the last CTA's
+// thread 0 with *total = the grid's sum; that thread has reset the word.
+#ifndef RD_NO_PACKED_SUM
+#define RD_PACKED_SUM 1
+#else
+#define RD_PACKED_SUM 0
+#endif
+template <bool ACQ_REL = false>
+__device__ __forceinline__ bool packed_arrive(unsigned* ticket, uint32_t a, uint32_t* total) {
+  unsigned long long old;
+  const unsigned long long add = ((unsigned long long)a << 32) | 1ull;
+  if constexpr (ACQ_REL)
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(ticket), "l"(add) : "memory");
+  else
+    asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(ticket), "l"(add) : "memory");
+  if ((uint32_t)old != gridDim.x - 1) return false;
+  *total = (uint32_t)(old >> 32) + a;
+  *reinterpret_cast<unsigned long long*>(ticket) = 0ull;   // reusable by the next launch
+  return true;
+}
+
 // a6: one partial per CTA, the last CTA to arrive folds them in index order.
 template <class OpT, int B>
 __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& args,
@@ -369,6 +395,21 @@ __device__ __forceinline__ void grid_combine(typename OpT::Acc a, const KArgs& a
   using Acc = typename OpT::Acc;
   if (gridDim.x == 1) {
     if (threadIdx.x < 32) finish_warp0<OpT>(a, args);
+    return;
+  }
+  if constexpr (RD_PACKED_SUM && PackedSum32<OpT>::value) {
+    __shared__ unsigned s_done;
+    __shared__ uint32_t s_total;
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      s_done = packed_arrive(args.ticket, a, &tot);
+      s_total = tot;
+      RD_TL(4);
+    }
+    __syncthreads();
+    if (!s_done) return;
+    if (threadIdx.x < 32) finish_warp0<OpT>(s_total, args);
+    if (threadIdx.x == 0) RD_TL(7);
     return;
   }
   __shared__ unsigned s_last;

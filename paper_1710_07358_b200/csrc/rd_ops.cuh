@@ -346,6 +346,15 @@ struct FloatSum<double> : Float64SumComp {
 template <class O, class = void> struct OrderFree : std::false_type {};
 template <class O> struct OrderFree<O, std::void_t<decltype(O::kOrderFree)>> : std::bool_constant<O::kOrderFree> {};
 
+// 32-bit integer + (int32 / uint32 sum and their compensated / exact aliases):
+// the grid combine adds every CTA's partial and counts the CTA in ONE 64-bit
+// atomic add on {partial << 32 | 1} (rd_kernels.cuh packed_arrive) -- the sum
+// wraps mod 2^32 in the high word (carries leave the 64 bits), the count in
+// the low word never carries -- so the last CTA has the total from its
+// atomic's return value: no slots to fold.
+template <class O> struct PackedSum32 : std::false_type {};
+template <bool S> struct PackedSum32<IntOp<uint32_t, RD_SUM, S>> : std::true_type {};
+
 template <class O, class = void> struct Blocked : std::false_type {};
 template <class O> struct Blocked<O, std::void_t<decltype(O::kBlocked)>> : std::bool_constant<O::kBlocked> {};
 

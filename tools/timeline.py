@@ -33,7 +33,8 @@ import inputs  # noqa: E402
 DT = {"int32": 0, "uint32": 1, "int64": 2, "float32": 3, "float64": 4}
 OPS = {"sum": 0, "prod": 1, "min": 2, "max": 3, "and": 4, "or": 5, "xor": 6, "argmin": 7, "argmax": 8,
        "sum_compensated": 9, "sum_exact": 10}
-TORCH_DT = {"int32": torch.int32, "float32": torch.float32, "float64": torch.float64, "int64": torch.int64}
+TORCH_DT = {"int32": torch.int32, "uint32": torch.uint32, "float32": torch.float32, "float64": torch.float64,
+            "int64": torch.int64}
 
 _flush = None
 
