@@ -408,6 +408,152 @@ __device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L
   }
 }
 
+// ------------------------------------------------------------------- bins
+// The fallback for groups the group paths cannot sum exactly (exponents
+// spread wider than one fp64 significand can hold: the `wide` workload, where
+// nearly every group fails): BINNED EXTRACTION after Demmel & Nguyen's
+// indexed summation (the technique of ReproBLAS), with enough bins and a
+// bounded number of additions that it is EXACT, not only reproducible.
+// Each thread keeps K fp64 bins with fixed exponents a_j = a_0 - j*W (W = 38):
+// bin j holds S_j = 1.5*2^(a_j) + (sum of the pieces it took), and every piece
+// is a multiple of its unit u_j = ulp(S_j) = 2^(a_j - 52). A term x passes
+// down the bins: t = fl(S_j + r); q = t - S_j (exact: Sterbenz); r = r - q
+// (exact: the error of rounding r to a multiple of u_j); S_j = t. Bounds that
+// keep every step exact: |x| <= 2^(a_0 + W - 53) (floor(log2|x|) <= a_0 - 16,
+// else the bins are re-anchored higher) and at most 4096 < 2^(51 - W)
+// additions between re-anchorings, so |S_j - 1.5*2^(a_j)| < 2^(a_j - 2) and
+// S_j never leaves its binade. What falls below the last bin's unit (r != 0
+// after bin K-1) is deposited into the warp's superaccumulator; when every
+// term's lowest bit is at least that unit (checked from the exponent fields,
+// per warp), the last bin is one plain add. Re-anchoring deposits each bin's
+// content S_j - 1.5*2^(a_j) (exact) into the superaccumulator. Per term: 3
+// DADD per bin but the last (1) -- 7 for fp32 (K = 3: 114 + 52 bits below
+// the anchor, the `wide` fp32 range 2^-63..2^41 with 5 bits to spare), 10 for
+// fp64 (K = 4) -- branch-free and independent of the order of the terms
+// (round 1's per-element TwoSum cascade: ~20 dependent FP64 ops per term).
+constexpr int kBinW = 38;                  // bits per bin
+constexpr int kBinHead = 54 - kBinW;       // bins take floor(log2|x|) <= a_0 - kBinHead
+constexpr int kBinSlack = 4;               // a new anchor leaves this many binades of room above the max
+constexpr int kBinMaxAdds = 4096;          // additions per bin between re-anchorings (< 2^(51 - kBinW))
+template <typename T> struct BinK;
+template <> struct BinK<float> { static constexpr int K = 3; };
+template <> struct BinK<double> { static constexpr int K = 4; };
+
+template <int K>
+struct Bins {
+  double s[K];   // S_j
+  int top;       // the largest floor(log2|x|) the bins take: a_0 - kBinHead
+  int count;     // terms added since the last (re)anchoring
+};
+// Each lane's bins live in shared memory (the warp's block, lane-strided: no
+// bank conflicts), not in registers: only the out-of-line fallback touches
+// them, and the hot loop keeps its registers (8-10 per thread otherwise).
+template <int K>
+struct WarpBins {
+  double s[K][32];
+  int top[32];
+  int count[32];
+};
+// the lowest anchor whose K bins are all normal doubles
+template <int K> __host__ __device__ constexpr int bins_min_a0() { return -1022 + (K - 1) * kBinW; }
+// the largest floor(log2|x|) any anchor takes (a_0 <= 1023)
+constexpr int kBinMaxTop = 1023 - kBinHead;
+
+__device__ __forceinline__ double bin_anchor(int a) {   // 1.5 * 2^a, a in [-1022, 1023]
+  return __hiloint2double(((a + 1023) << 20) | 0x80000, 0);
+}
+template <int K>
+__device__ __forceinline__ void bins_init(WarpBins<K>* wb) {
+  constexpr int a0 = bins_min_a0<K>();
+  const int ln = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < K; ++j) wb->s[j][ln] = bin_anchor(a0 - j * kBinW);
+  wb->top[ln] = a0 - kBinHead;
+  wb->count[ln] = 0;
+}
+template <int K>
+__device__ __forceinline__ Bins<K> bins_load(const WarpBins<K>* wb) {
+  const int ln = threadIdx.x & 31;
+  Bins<K> bn;
+#pragma unroll
+  for (int j = 0; j < K; ++j) bn.s[j] = wb->s[j][ln];
+  bn.top = wb->top[ln];
+  bn.count = wb->count[ln];
+  return bn;
+}
+template <int K>
+__device__ __forceinline__ void bins_store(WarpBins<K>* wb, const Bins<K>& bn) {
+  const int ln = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < K; ++j) wb->s[j][ln] = bn.s[j];
+  wb->top[ln] = bn.top;
+  wb->count[ln] = bn.count;
+}
+// bin j's content, exact (S_j and 1.5 * 2^(a_j) are within a factor 2)
+template <int K>
+__device__ __forceinline__ double bin_value(const Bins<K>& bn, int j) {
+  return __dsub_rn(bn.s[j], bin_anchor(bn.top + kBinHead - j * kBinW));
+}
+
+// One group of GL finite terms (gmax >= every floor(log2|x|), gmax <=
+// kBinMaxTop; glow <= the exponent of every nonzero term's lowest bit) into
+// this lane's bins; called from the out-of-line group fallbacks. Returns the
+// flags.
+template <typename T, int K, int GL>
+__device__ __forceinline__ uint32_t bins_group(WarpBins<K>* wb, uint32_t flags, const ExVals<GL>& xs, int gmax,
+                                               int glow, long long* w) {
+  const unsigned mask = __activemask();
+  Bins<K> bn = bins_load(wb);
+  if (gmax > bn.top || bn.count > kBinMaxAdds - GL) {   // re-anchor (per lane, rare)
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const double d = bin_value(bn, j);
+      if (d != 0.0) sacc_add<T>(w, d);
+    }
+    int a0 = bn.top + kBinHead;
+    if (gmax > bn.top) a0 = min(max(gmax + kBinHead + kBinSlack, bins_min_a0<K>()), 1023);
+#pragma unroll
+    for (int j = 0; j < K; ++j) bn.s[j] = bin_anchor(a0 - j * kBinW);
+    bn.top = a0 - kBinHead;
+    bn.count = 0;
+  }
+  __syncwarp(mask);
+  bn.count += GL;
+  bool nz = false;                                   // some term is not -0.0
+#pragma unroll
+  for (int l = 0; l < GL; ++l) nz |= (uint64_t)__double_as_longlong(xs.v[l]) != kNegZeroBits;
+  if (nz) flags |= kXNotNegZero;
+  const int low = bn.top + kBinHead - (K - 1) * kBinW - 52;   // exponent of the last bin's unit
+  if (__all_sync(mask, glow >= low)) {
+    // every term is a multiple of the last bin's unit: nothing falls below it
+#pragma unroll
+    for (int l = 0; l < GL; ++l) {
+      double r = xs.v[l];
+#pragma unroll
+      for (int j = 0; j < K - 1; ++j) {
+        const double t = __dadd_rn(bn.s[j], r);
+        r = __dsub_rn(r, __dsub_rn(t, bn.s[j]));
+        bn.s[j] = t;
+      }
+      bn.s[K - 1] = __dadd_rn(bn.s[K - 1], r);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < GL; ++l) {
+      double r = xs.v[l];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const double t = __dadd_rn(bn.s[j], r);
+        r = __dsub_rn(r, __dsub_rn(t, bn.s[j]));
+        bn.s[j] = t;
+      }
+      if (r != 0.0) sacc_add<T>(w, r);
+    }
+  }
+  bins_store(wb, bn);
+  return flags;
+}
+
 // The per-element levels for a group whose group speculation failed, in
 // pieces of P elements: each piece speculates (fold_vec_exact) and replays on
 // its own, so one inexact element replays P elements, not the whole group --
@@ -425,13 +571,21 @@ __device__ __forceinline__ void elementwise_pieces(ExState<E, GL>& st, const ExV
   }
 }
 
-// fp32 data, the per-element path for one group whose group speculation
-// failed, out of line (one copy per kernel): fold_vec_exact's levels --
-// tested adds into a0, then two TwoSum levels, then the element replay --
-// per 4 elements.
-template <int E, int GL>
-__device__ __noinline__ ExState<E, GL> exact32_elementwise(ExState<E, GL> st, const ExVals<GL> xs, long long* w) {
-  elementwise_pieces<float, E, GL, (GL < 4 ? GL : 4)>(st, xs, w);
+// fp32 data, one group the group path could not take, out of line (one
+// copy per kernel, one cold call site per group): inf/NaN terms in the warp
+// -> fold_vec_exact's per-element levels (tested adds into a0, two TwoSum
+// levels, the element replay) per 4 elements, which keep the flags; else the
+// bins. mx / mn: the group's max |bits| and min |bits| - 1 (zeros skipped).
+template <int E, int GL, int K>
+__device__ __noinline__ ExState<E, GL> exact32_fallback(ExState<E, GL> st, const ExVals<GL> xs, WarpBins<K>* wb,
+                                                        uint32_t mx, uint32_t mn, long long* w) {
+  if (__any_sync(__activemask(), mx >= 0x7f800000u)) {
+    elementwise_pieces<float, E, GL, (GL < 4 ? GL : 4)>(st, xs, w);
+    return st;
+  }
+  // floor(log2|x|) <= (mx >> 23) - 127; every nonzero term's lowest bit is at
+  // least 2^((mn >> 23) - 150) (mn's field may be one below the term's)
+  st.flags = bins_group<float, K, GL>(wb, st.flags, xs, (int)(mx >> 23) - 127, (int)(mn >> 23) - 150, w);
   return st;
 }
 
@@ -445,14 +599,16 @@ __device__ __noinline__ ExState<E, GL> exact32_elementwise(ExState<E, GL> st, co
 // integer ops (|b|, max |b|, |b| - 1, min) -- 1.5 FP64 ops per element
 // instead of the per-element test's 5: the FP64 work and its power were
 // what held the sustained exact sum at 85% of the read probe.
-// The max |b| < inf test sends inf/NaN groups, the e_min (from |b| - 1, so
-// zeros drop out and subnormals count as exponent 0) test wide or subnormal
-// groups, and an inexact add into a0 any group, to the per-element path.
-template <int E, int GL>
-__device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], int g, const uint32_t (&b)[GL], long long* w,
-                                                   uint32_t& flags) {
+// Decisions are per warp, with ONE vote on the common path: inf/NaN terms
+// send the group to the per-element path (which keeps the flags); an
+// exponent spread past the bound (e_min from |b| - 1, so zeros drop out and
+// subnormals count as exponent 0) or an inexact add into a0 to the bins.
+template <int E, int GL, int K>
+__device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], WarpBins<K>* wb, int g, const uint32_t (&b)[GL],
+                                                   long long* w, uint32_t& flags) {
   static_assert(GL == 4 || GL == 8 || GL == 16, "group of 4, 8 or 16 floats");
   constexpr int kMaxSpread = 29 - (GL == 4 ? 2 : GL == 8 ? 3 : 4);
+  const unsigned mask = __activemask();
   uint32_t mx = 0, mn = 0xffffffffu;
   double x[GL];
 #pragma unroll
@@ -462,12 +618,13 @@ __device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], int g, const uin
     mn = min(mn, a - 1u);                            // zero -> 0xffffffff: no effect
     x[l] = (double)__uint_as_float(b[l]);            // exact widening
   }
+  const bool special = mx >= 0x7f800000u;
+  const bool wide = (int)(mx >> 23) - (int)(mn >> 23) > kMaxSpread;
   const double s = tree_sum<GL>(x);                  // exact when the spread test holds
   Ex& q = ex[g % E];
   const double t = __dadd_rn(q.a0, s);
-  const bool bad = (mx >= 0x7f800000u) | ((int)(mx >> 23) - (int)(mn >> 23) > kMaxSpread) |
-                   (__dsub_rn(t, q.a0) != s) | (__dsub_rn(t, s) != q.a0);
-  if (__builtin_expect(!__any_sync(__activemask(), bad), 1)) {
+  const bool bad = special | wide | (__dsub_rn(t, q.a0) != s) | (__dsub_rn(t, s) != q.a0);
+  if (__builtin_expect(!__any_sync(mask, bad), 1)) {
     q.a0 = t;
     return;
   }
@@ -478,24 +635,59 @@ __device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], int g, const uin
   ExVals<GL> v;
 #pragma unroll
   for (int l = 0; l < GL; ++l) v.v[l] = x[l];
-  st = exact32_elementwise<E, GL>(st, v, w);
+  st = exact32_fallback<E, GL, K>(st, v, wb, mx, mn, w);
 #pragma unroll
   for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
   flags = st.flags;
 }
 
-// fp64 data, the per-element path for one group (out of line), per 2 elements
-template <int E, int GL>
-__device__ __noinline__ ExState<E, GL> exact64_elementwise(ExState<E, GL> st, const ExVals<GL> xs, long long* w) {
-  elementwise_pieces<double, E, GL, 2>(st, xs, w);
+// fp64 data, one group the group path could not take, out of line (one
+// copy per kernel): the exponent fields are recomputed with the low words
+// (a subnormal below 2^-1042 has a zero high word but counts as exponent 0);
+// inf/NaN terms or a term past the bins' range (> 2^1007) in the warp -> the
+// per-element levels per 2 elements; else the bins.
+template <int E, int GL, int K>
+__device__ __noinline__ ExState<E, GL> exact64_fallback(ExState<E, GL> st, const ExVals<GL> xs, WarpBins<K>* wb,
+                                                        long long* w) {
+  uint32_t xmax = 0, xmin = 0xffffffffu;
+#pragma unroll
+  for (int l = 0; l < GL; ++l) {
+    const uint32_t xh = ((uint32_t)__double2hiint(xs.v[l]) & 0x7fffffffu) | min((uint32_t)__double2loint(xs.v[l]), 1u);
+    xmax = max(xmax, xh);
+    xmin = min(xmin, xh - 1u);                       // zero -> 0xffffffff: no effect
+  }
+  if (__any_sync(__activemask(), (xmax >> 20) > (uint32_t)(1023 + kBinMaxTop))) {
+    elementwise_pieces<double, E, GL, 2>(st, xs, w);
+    return st;
+  }
+  // floor(log2|x|) <= (xmax >> 20) - 1023; every nonzero term's lowest bit is
+  // at least 2^((xmin >> 20) - 1075)
+  st.flags = bins_group<double, K, GL>(wb, st.flags, xs, (int)(xmax >> 20) - 1023, (int)(xmin >> 20) - 1075, w);
   return st;
+}
+
+template <int E, int GL, int K>
+__device__ __forceinline__ void exact64_fallback_call(Ex (&ex)[E], uint32_t& flags, const double (&x)[GL],
+                                                      WarpBins<K>* wb, long long* w) {
+  ExState<E, GL> st;
+#pragma unroll
+  for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
+  st.flags = flags;
+  ExVals<GL> v;
+#pragma unroll
+  for (int l = 0; l < GL; ++l) v.v[l] = x[l];
+  st = exact64_fallback<E, GL, K>(st, v, wb, w);
+#pragma unroll
+  for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
+  flags = st.flags;
 }
 
 // fp64 data, a GROUP of GL elements into one expansion (a0, a1): the GL
 // errors of the adds into a0 are summed in a tree and ONE tested add puts that
 // sum into a1 (as spec2's test). The error tree is exact when every error is
-// a multiple of 2^m (m: the smallest ulp among the terms and the running sums
-// they meet) and below half an ulp of the largest running sum: the exponent
+// a multiple of 2^m (m: the smallest ulp among the terms and the starting a0
+// -- every running sum, rounded or not, is a multiple of the finest of their
+// grids) and below half an ulp of the largest running sum: the exponent
 // spread <= 54 - log2(GL) -- or trivially when every error is 0 (e.g. terms
 // on a common grid, such as the normalish workload's multiples of 2^-24).
 // Two forms, chosen per warp BEFORE the group work from facts the terms and
@@ -510,46 +702,58 @@ __device__ __noinline__ ExState<E, GL> exact64_elementwise(ExState<E, GL> st, co
 //    wasted speculation. (Speculating Fast2Sum and replaying on failure had
 //    cost zero-mean fp64 data 15-29%: with 32 lanes per warp some lane's sum
 //    is nearly always near zero.)
-// inf/NaN terms or a spread of the terms alone past the bound: the
-// per-element levels straight away; an overflow, a spread past the bound
-// (with the running sums) with a nonzero error, or an inexact a1 add: the
-// group is replayed through them. Both out of line.
-template <int E, int GL>
-__device__ __forceinline__ void fold_group_exact64(Ex (&ex)[E], int g, const double (&x)[GL], long long* w,
-                                                   uint32_t& flags) {
+// Per warp: inf/NaN terms or a term above the bins' range (> 2^1007): the
+// per-element levels (out of line); a spread of the terms alone past the
+// bound: the bins (no group work to throw away); an overflow, a spread past
+// the bound (with the running sums) with a nonzero error, or an inexact a1
+// add: the bins after the group work, told floor(log2|x|) <= (xmax >> 20) -
+// 1023 and that every nonzero term's lowest bit is >= 2^((xmin >> 20) - 1075).
+template <int E, int GL, int K>
+__device__ __forceinline__ void fold_group_exact64(Ex (&ex)[E], WarpBins<K>* wb, int g, const double (&x)[GL],
+                                                   long long* w, uint32_t& flags) {
   static_assert(GL == 4 || GL == 8, "group of 4 or 8 doubles");
   constexpr int kLog2GL = (GL == 4 ? 2 : 3);
   constexpr int kMaxSpread = 54 - kLog2GL;
   const unsigned mask = __activemask();
   Ex& q = ex[g % E];
-  uint32_t xmax = 0, xmin = 0xffffffffu;
+  // exponent fields from the high words: xmax = max |hi|, xmin = SIGNED min
+  // of |hi| - 1, which is -1 exactly when some high word is 0 -- a zero, or a
+  // subnormal below 2^-1042 whose bits are all in the low word and which must
+  // count as exponent 0 (else an error tree that mixes it with errors 2^53
+  // larger passes the spread test). Only such groups read the low words, in
+  // the rare branch, which recomputes the fields with zeros dropped out.
+  uint32_t xmax = 0;
+  int xmin_s = 0x7fffffff;
 #pragma unroll
   for (int l = 0; l < GL; ++l) {
     const uint32_t xh = (uint32_t)__double2hiint(x[l]) & 0x7fffffffu;
     xmax = max(xmax, xh);
-    xmin = min(xmin, xh - 1u);                       // zero -> 0xffffffff: no effect
+    xmin_s = min(xmin_s, (int)xh - 1);
   }
-  // inf/NaN terms, or terms too far apart for any exact error tree: the
-  // per-element levels straight away (no group work to throw away)
-  if (__builtin_expect(__any_sync(mask, (xmax >= 0x7ff00000u) |
-                                            ((int)(xmax >> 20) - (int)(xmin >> 20) > kMaxSpread)), 0)) {
-    ExState<E, GL> st;
+  uint32_t xmin = (uint32_t)xmin_s;
+  const bool special = (xmax >> 20) > (uint32_t)(1023 + kBinMaxTop);   // inf/NaN, or past the bins
+  const bool wide = (int)(xmax >> 20) - (xmin_s >> 20) > kMaxSpread;
+  if (__builtin_expect(__any_sync(mask, special | wide | (xmin_s < 0)), 0)) {
+    bool out = __any_sync(mask, special | wide);
+    if (!out) {                                      // zeros (or subnormals below 2^-1042) only
+      xmin = 0xffffffffu;
 #pragma unroll
-    for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
-    st.flags = flags;
-    ExVals<GL> v;
-#pragma unroll
-    for (int l = 0; l < GL; ++l) v.v[l] = x[l];
-    st = exact64_elementwise<E, GL>(st, v, w);
-#pragma unroll
-    for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
-    flags = st.flags;
-    return;
+      for (int l = 0; l < GL; ++l) {
+        const uint32_t xh = ((uint32_t)__double2hiint(x[l]) & 0x7fffffffu) | min((uint32_t)__double2loint(x[l]), 1u);
+        xmin = min(xmin, xh - 1u);                   // zero -> 0xffffffff: no effect
+      }
+      out = __any_sync(mask, (int)(xmax >> 20) - (int)(xmin >> 20) > kMaxSpread);
+    }
+    if (out) {                                       // the fallback: per element or the bins, no group work
+      exact64_fallback_call<E, GL, K>(ex, flags, x, wb, w);
+      return;
+    }
+    // zeros only: the group work with the zeros dropped out of xmin
   }
   const uint32_t a0h = (uint32_t)__double2hiint(q.a0) & 0x7fffffffu;
   const bool fast = __all_sync(mask, (a0h >> 20) >= (xmax >> 20) + 1 + kLog2GL);
   double a = q.a0, e[GL];
-  uint32_t smax = 0, amin = 0xffffffffu;
+  uint32_t smax = 0, amin = 0xffffffffu;   // amin: the starting a0 (the running sums' grids follow from it and the terms)
   if (fast) {
 #pragma unroll
     for (int l = 0; l < GL; ++l) {
@@ -559,9 +763,9 @@ __device__ __forceinline__ void fold_group_exact64(Ex (&ex)[E], int g, const dou
       smax = max(smax, (uint32_t)__double2hiint(a) & 0x7fffffffu);
     }
   } else {
+    amin = (a0h | min((uint32_t)__double2loint(q.a0), 1u)) - 1u;   // a zero a0 drops out
 #pragma unroll
     for (int l = 0; l < GL; ++l) {
-      amin = min(amin, ((uint32_t)__double2hiint(a) & 0x7fffffffu) - 1u);   // zero sums drop out
       double sl;
       two_sum(a, x[l], sl, e[l]);
       a = sl;
@@ -574,7 +778,7 @@ __device__ __forceinline__ void fold_group_exact64(Ex (&ex)[E], int g, const dou
   const uint32_t mn = min(xmin, amin);
   const double se = tree_sum<GL>(e);
   const double t = __dadd_rn(q.a1, se);
-  const bool bad = (smax >= 0x7ff00000u) | (xmax >= 0x7ff00000u) |
+  const bool bad = (smax >= 0x7ff00000u) |
                    (nz & ((int)(smax >> 20) - (int)(mn >> 20) > kMaxSpread)) |
                    (__dsub_rn(t, q.a1) != se) | (__dsub_rn(t, se) != q.a1);
   if (__builtin_expect(!__any_sync(mask, bad), 1)) {
@@ -582,17 +786,7 @@ __device__ __forceinline__ void fold_group_exact64(Ex (&ex)[E], int g, const dou
     q.a1 = t;
     return;
   }
-  ExState<E, GL> st;
-#pragma unroll
-  for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
-  st.flags = flags;
-  ExVals<GL> v;
-#pragma unroll
-  for (int l = 0; l < GL; ++l) v.v[l] = x[l];
-  st = exact64_elementwise<E, GL>(st, v, w);
-#pragma unroll
-  for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
-  flags = st.flags;
+  exact64_fallback_call<E, GL, K>(ex, flags, x, wb, w);
 }
 
 // round the normalised words (value = sum w[k] 2^(32k) * 2^kLsb) once; returns the float's bits
@@ -815,9 +1009,10 @@ __device__ __forceinline__ void sacc_flush_warp(long long* w, const double (&d)[
 // a3-a5, shared by the exact kernels: the expansions -> warp
 // superaccumulators -> the CTA's carried-digit sums in cta[0..NW) (< 2^35 per
 // word) and its flags in cta[NW]. Ends with __syncthreads.
-template <typename T, int B, int E>
-__device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
-                                                unsigned& s_flags, long long* cta) {
+template <typename T, int B, int E, int K>
+__device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], const WarpBins<K>* wbins, uint32_t flags,
+                                                long long (*sacc)[ExactTraits<T>::kWords], unsigned& s_flags,
+                                                long long* cta) {
   constexpr int NW = ExactTraits<T>::kWords;
   constexpr int NWARP = B / 32;
   const int warp = threadIdx.x >> 5, ln = threadIdx.x & 31;
@@ -827,7 +1022,7 @@ __device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], uint32_t flags, lon
   // has seen a term other than -0.0 is never -0.0 again (x + -x = +0), so a0
   // alone decides reading R2's "every term is -0.0".
   __syncwarp();
-  double dv[3 * E];
+  double dv[3 * E + K];
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     if ((uint64_t)__double_as_longlong(ex[j].a0) != kNegZeroBits) flags |= kXNotNegZero;
@@ -835,7 +1030,13 @@ __device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], uint32_t flags, lon
     dv[3 * j + 1] = ex[j].a1;
     dv[3 * j + 2] = ex[j].a2;
   }
-  sacc_flush_warp<T, 3 * E>(w, dv);
+#pragma unroll
+  {
+    const Bins<K> bn = bins_load(&wbins[warp]);
+#pragma unroll
+    for (int j = 0; j < K; ++j) dv[3 * E + j] = bin_value(bn, j);   // the bins' contents (flags set by bins_group)
+  }
+  sacc_flush_warp<T, 3 * E + K>(w, dv);
   flags = __reduce_or_sync(0xffffffffu, flags);
   if (ln == 0 && flags) atomicOr(&s_flags, flags);
   __syncwarp();
@@ -881,13 +1082,14 @@ __device__ __forceinline__ void exact_emit(long long* words, unsigned flags, con
 
 // a3-a7 for the persistent grids: the CTA's words go to workspace slot
 // blockIdx; the last CTA (atomic ticket) adds the G slots and emits.
-template <typename T, int B, int E>
-__device__ __forceinline__ void exact_finish(Ex (&ex)[E], uint32_t flags, long long (*sacc)[ExactTraits<T>::kWords],
+template <typename T, int B, int E, int K>
+__device__ __forceinline__ void exact_finish(Ex (&ex)[E], const WarpBins<K>* wbins, uint32_t flags,
+                                             long long (*sacc)[ExactTraits<T>::kWords],
                                              long long* tot, unsigned& s_flags, unsigned& s_last,
                                              const XArgs& args) {
   constexpr int NW = ExactTraits<T>::kWords;
   long long* slot = args.partials + (size_t)blockIdx.x * (NW + 1);
-  exact_cta_words<T, B, E>(ex, flags, sacc, s_flags, tot);
+  exact_cta_words<T, B, E, K>(ex, wbins, flags, sacc, s_flags, tot);
   if (threadIdx.x <= NW) __stcg(slot + threadIdx.x, tot[threadIdx.x]);
   // a6: last CTA adds the G slots
   __syncthreads();
@@ -940,12 +1142,12 @@ __device__ __forceinline__ long long dsmem_load_i64(const long long* local, unsi
   return v;
 }
 
-template <typename T, int B, int E>
-__device__ __forceinline__ void exact_finish_cluster(Ex (&ex)[E], uint32_t flags,
+template <typename T, int B, int E, int K>
+__device__ __forceinline__ void exact_finish_cluster(Ex (&ex)[E], const WarpBins<K>* wbins, uint32_t flags,
                                                      long long (*sacc)[ExactTraits<T>::kWords], long long* cta,
                                                      unsigned& s_flags, const XArgs& args) {
   constexpr int NW = ExactTraits<T>::kWords;
-  exact_cta_words<T, B, E>(ex, flags, sacc, s_flags, cta);
+  exact_cta_words<T, B, E, K>(ex, wbins, flags, sacc, s_flags, cta);
   cluster_sync();
   if (cluster_ctarank() == 0) {
     const unsigned G = cluster_nctarank();
@@ -977,12 +1179,14 @@ __device__ __forceinline__ void exact_finish_cluster(Ex (&ex)[E], uint32_t flags
 // there. Without it the warp stayed split after the first divergent replay
 // and ran the loop ~2 lanes at a time (ncu: 2.0 avg threads per F2F).
 template <typename T, int B, int U, int E>
-__device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E], long long* w, uint32_t& flags) {
+__device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E], WarpBins<BinK<T>::K>* wb,
+                                                  long long* w, uint32_t& flags) {
   constexpr int VB = 32;
   constexpr int L = VB / (int)sizeof(T);
   const int ln = threadIdx.x & 31;
 #pragma unroll
   for (int j = 0; j < E; ++j) ex[j] = Ex{-0.0, -0.0, -0.0};
+  bins_init(wb);
   const uint64_t tid = (uint64_t)blockIdx.x * B + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * B;
   const unsigned char* body = args.x + args.head * sizeof(T);
@@ -996,7 +1200,7 @@ __device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E]
     for (int u = 0; u < U; ++u) v[u] = ldg_stream<VB>(body + (i + (uint64_t)u * stride) * VB);
     if constexpr (sizeof(T) == 4) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) fold_group_exact32<E, L>(ex, u, v[u].w, w, flags);
+      for (int u = 0; u < U; ++u) fold_group_exact32<E, L>(ex, wb, u, v[u].w, w, flags);
     } else if constexpr (U % 2 == 0) {
       // fp64: groups of 8 (two 32-byte vectors)
 #pragma unroll
@@ -1007,7 +1211,7 @@ __device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E]
           xs[l] = lane<T, VB>(v[u], l);
           xs[L + l] = lane<T, VB>(v[u + 1], l);
         }
-        fold_group_exact64<E, 2 * L>(ex, u / 2, xs, w, flags);
+        fold_group_exact64<E, 2 * L>(ex, wb, u / 2, xs, w, flags);
       }
     } else {
 #pragma unroll
@@ -1015,7 +1219,7 @@ __device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E]
         double xs[L];
 #pragma unroll
         for (int l = 0; l < L; ++l) xs[l] = lane<T, VB>(v[u], l);
-        fold_group_exact64<E, L>(ex, u, xs, w, flags);
+        fold_group_exact64<E, L>(ex, wb, u, xs, w, flags);
       }
     }
     __syncwarp();
@@ -1023,7 +1227,7 @@ __device__ __forceinline__ void exact_vector_body(const XArgs& args, Ex (&ex)[E]
   for (; i < nvec; i += stride) {
     Vec<VB> v = ldg_stream<VB>(body + i * VB);
     if constexpr (sizeof(T) == 4) {
-      fold_group_exact32<E, L>(ex, 0, v.w, w, flags);
+      fold_group_exact32<E, L>(ex, wb, 0, v.w, w, flags);
     } else {
       double xs[L];
 #pragma unroll
@@ -1048,10 +1252,11 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_kernel(const __grid_constant
   for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
   if (threadIdx.x == 0) s_flags = 0;
   __syncthreads();
+  __shared__ WarpBins<BinK<T>::K> wbins[NWARP];
   Ex ex[E];
   uint32_t flags = 0;
-  exact_vector_body<T, B, U, E>(args, ex, sacc[threadIdx.x >> 5], flags);
-  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
+  exact_vector_body<T, B, U, E>(args, ex, &wbins[threadIdx.x >> 5], sacc[threadIdx.x >> 5], flags);
+  exact_finish<T, B, E>(ex, wbins, flags, sacc, tot, s_flags, s_last, args);
 }
 
 // The same on a grid that is ONE thread-block cluster (<= 16 CTAs): AUTO's
@@ -1067,10 +1272,11 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_cluster_kernel(const __grid_
   for (int i = threadIdx.x; i < NWARP * NW; i += B) (&sacc[0][0])[i] = 0;
   if (threadIdx.x == 0) s_flags = 0;
   __syncthreads();
+  __shared__ WarpBins<BinK<T>::K> wbins[NWARP];
   Ex ex[E];
   uint32_t flags = 0;
-  exact_vector_body<T, B, U, E>(args, ex, sacc[threadIdx.x >> 5], flags);
-  exact_finish_cluster<T, B, E>(ex, flags, sacc, cta, s_flags, args);
+  exact_vector_body<T, B, U, E>(args, ex, &wbins[threadIdx.x >> 5], sacc[threadIdx.x >> 5], flags);
+  exact_finish_cluster<T, B, E>(ex, wbins, flags, sacc, cta, s_flags, args);
 }
 
 // The bulk-copy form (like rd_bulk_kernel): one producer lane streams
@@ -1094,6 +1300,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
   uint64_t* empty = full + STAGES;
   uint32_t* st_bytes = reinterpret_cast<uint32_t*>(empty + STAGES);   // 0 = no more chunks
   __shared__ long long sacc[B / 32][NW];
+  __shared__ WarpBins<BinK<T>::K> wbins[B / 32];
   __shared__ long long tot[B];
   __shared__ unsigned s_flags, s_last;
 
@@ -1111,6 +1318,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
   Ex ex[E];
 #pragma unroll
   for (int j = 0; j < E; ++j) ex[j] = Ex{-0.0, -0.0, -0.0};
+  bins_init(&wbins[warp]);
   uint32_t flags = 0;
   const unsigned char* body = args.x + args.head * sizeof(T);
   const uint64_t body_bytes = args.nvec * 16;
@@ -1162,7 +1370,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
 #pragma unroll
           for (int k = 0; k < PER_THREAD; k += 2) {
             const uint32_t b8[8] = {v[k].x, v[k].y, v[k].z, v[k].w, v[k + 1].x, v[k + 1].y, v[k + 1].z, v[k + 1].w};
-            fold_group_exact32<E, 8>(ex, k / 2, b8, w, flags);
+            fold_group_exact32<E, 8>(ex, &wbins[warp], k / 2, b8, w, flags);
           }
         } else if constexpr (sizeof(T) == 8 && PER_THREAD % 4 == 0) {
           // fp64: groups of 8 (four LDS.128)
@@ -1175,7 +1383,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
               d8[2 * j] = lane<T, 16>(q, 0);
               d8[2 * j + 1] = lane<T, 16>(q, 1);
             }
-            fold_group_exact64<E, 8>(ex, k / 4, d8, w, flags);
+            fold_group_exact64<E, 8>(ex, &wbins[warp], k / 4, d8, w, flags);
           }
         } else {
 #pragma unroll
@@ -1212,7 +1420,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
     }
   }
   pdl_trigger();
-  exact_finish<T, B, E>(ex, flags, sacc, tot, s_flags, s_last, args);
+  exact_finish<T, B, E>(ex, wbins, flags, sacc, tot, s_flags, s_last, args);
 }
 
 // Fold `count` exact records (any order gives the same integer): one CTA.

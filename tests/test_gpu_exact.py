@@ -270,3 +270,70 @@ def test_exact_carry_chains(rd, dtype):
             assert same(val(got), want), (dtype, len(x), variant)
         rec = rd.reduce_exact_partial(xd)
         assert same(val(rd.combine_exact_records(rec, dtype)), want)
+
+
+def _ramp(n, dtype, lo, hi, rng, up=True):
+    """Magnitudes that grow (or shrink) along the array: every thread's grid-stride
+    share sees its maximum grow, so the bins re-anchor again and again (or, shrinking,
+    terms fall below the last bin and are deposited)."""
+    e = np.linspace(lo, hi, n) if up else np.linspace(hi, lo, n)
+    m = rng.random(n) + 0.5
+    return (rng.choice([-1.0, 1.0], n) * np.ldexp(m, np.floor(e).astype(int))).astype(dtype)
+
+
+@pytest.mark.parametrize("dtype", FLT)
+def test_exact_bins(rd, dtype):
+    """The binned-extraction fallback (rd_exact.cuh bins_group): re-anchoring on a
+    growing maximum, terms below the last bin, the 4096-addition limit (one CTA, long
+    per-thread runs), groups that alternate between the group path and the bins in
+    one thread -- bit-exact against the oracle on every variant."""
+    rng = np.random.default_rng(11)
+    big = 120 if dtype == "float32" else 1000
+    small = -140 if dtype == "float32" else -1070
+    cases = [
+        _ramp((1 << 20) + 3, dtype, -60, 60, rng),
+        _ramp((1 << 20) + 3, dtype, -60, 60, rng, up=False),
+        _ramp((1 << 18) + 1, dtype, small, big, rng),
+        _ramp((1 << 18) + 1, dtype, small, big, rng, up=False),
+    ]
+    mixed = inputs.generate((1 << 20) + 5, dtype, "u01", seed=2)
+    idx = rng.integers(0, mixed.size, mixed.size // 97)
+    mixed[idx] = inputs.generate(idx.size, dtype, "wide", seed=3)
+    cases.append(mixed)
+    for x in cases:
+        want = oracle.reduce(x, "sum_exact").value
+        xd = to_dev(x, 3)
+        for variant in ("auto", "vector", "bulk"):
+            assert same(val(rd.reduce_ex(xd, "sum_exact", variant=variant)[0]), want), (dtype, variant)
+    # long per-thread runs: one CTA over 2^22 wide terms -> > 4096 additions per bin
+    x = inputs.generate(1 << 22, dtype, "wide", seed=8)
+    want = oracle.reduce(x, "sum_exact").value
+    xd = to_dev(x)
+    for variant in ("vector", "bulk"):
+        assert same(val(rd.reduce_ex(xd, "sum_exact", variant=variant, grid=1)[0]), want), variant
+
+
+def test_exact_fp64_subnormal_high_word_zero(rd):
+    """A subnormal double below 2^-1042 has a zero high word. The fp64 group path's
+    exponent-spread test reads high words, so it must not take such a term for a zero:
+    here 2^-900 + 2^-1060 + (2^-900 + 2^-952) makes the group's error tree inexact
+    (2^-952 + 2^-1060 rounds), and the exact sum's last bit depends on the 2^-1060."""
+    a, t, b = 2.0 ** -900, 2.0 ** -1060, 2.0 ** -900 + 2.0 ** -952
+    rng = np.random.default_rng(4)
+    for pos in ([0, 1, 2], [0, 1, 1024], [2, 0, 1], [1024, 1025, 0]):
+        for n in (4096, 1 << 16, (1 << 20) + 8):
+            x = np.zeros(n, np.float64)
+            x[pos] = (a, t, b)
+            want = oracle.reduce(x, "sum_exact").value
+            xd = to_dev(x)
+            for variant in ("auto", "vector", "bulk"):
+                assert same(val(rd.reduce_ex(xd, "sum_exact", variant=variant)[0]), want), (pos, n, variant)
+    # randomised: terms near 2^-900 with 52-bit mantissas and high-word-zero subnormals
+    n = (1 << 20) + 3
+    x = np.ldexp(rng.random(n) + 1.0, -900) * rng.choice([-1.0, 1.0], n)
+    sub = rng.random(n) < 0.3
+    x[sub] = np.ldexp(rng.integers(1, 1 << 30, sub.sum()).astype(np.float64), -1074)
+    want = oracle.reduce(x, "sum_exact").value
+    xd = to_dev(x, 1)
+    for variant in ("auto", "vector", "bulk"):
+        assert same(val(rd.reduce_ex(xd, "sum_exact", variant=variant)[0]), want), variant

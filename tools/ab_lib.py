@@ -99,6 +99,8 @@ if __name__ == "__main__":
     for dtype in ("float32", "int32", "float64", "int64", "uint32"):
         xs[dtype] = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
         inputs.fill_device(xs[dtype], os.environ.get("AB_WORKLOAD", "u01") if dtype.startswith("float") else "int_small", seed=1)
-    for rnd in range(2):                      # interleaved twice: clock drift shows up
-        for p in sys.argv[1:]:
-            print(json.dumps({"lib": os.path.basename(p), "round": rnd, **run(p, xs)}), flush=True)
+    libs = sys.argv[1:]
+    rounds = int(os.environ.get("AB_ROUNDS", "2"))
+    for rnd in range(rounds):                 # ABBA...: clock / power drift cancels in the mean
+        for p in (libs if rnd % 2 == 0 else libs[::-1]):
+            print(json.dumps({"lib": os.path.relpath(p, ROOT), "round": rnd, **run(p, xs)}), flush=True)
