@@ -436,8 +436,8 @@ constexpr int kBinHead = 54 - kBinW;       // bins take floor(log2|x|) <= a_0 - 
 constexpr int kBinSlack = 4;               // a new anchor leaves this many binades of room above the max
 constexpr int kBinMaxAdds = 4096;          // additions per bin between re-anchorings (< 2^(51 - kBinW))
 template <typename T> struct BinK;
-template <> struct BinK<float> { static constexpr int K = 3; };
-template <> struct BinK<double> { static constexpr int K = 4; };
+template <> struct BinK<float> { static constexpr int K = 8; };    // 52 + 7 * 38 bits: every fp32 exponent
+template <> struct BinK<double> { static constexpr int K = 8; };
 
 template <int K>
 struct Bins {
@@ -499,59 +499,98 @@ __device__ __forceinline__ double bin_value(const Bins<K>& bn, int j) {
 // kBinMaxTop; glow <= the exponent of every nonzero term's lowest bit) into
 // this lane's bins; called from the out-of-line group fallbacks. Returns the
 // flags.
+// KE of this lane's K bins, straight from / to shared memory, every term a
+// multiple of bin KE-1's unit, so nothing falls below it and the last bin is
+// one plain add: 3 (KE - 1) + 1 DADD per term
+constexpr int kBinPre = 4;                 // bins loaded at entry, before the checks
+template <int K, int KE, int GL>
+__device__ __forceinline__ void bins_run(WarpBins<K>* wb, const ExVals<GL>& xs, const double (&pre)[kBinPre]) {
+  const int ln = threadIdx.x & 31;
+  double s[KE];
+#pragma unroll
+  for (int j = 0; j < KE; ++j) s[j] = j < kBinPre ? pre[j < kBinPre ? j : 0] : wb->s[j][ln];
+#pragma unroll
+  for (int l = 0; l < GL; ++l) {
+    double r = xs.v[l];
+#pragma unroll
+    for (int j = 0; j < KE - 1; ++j) {
+      const double t = __dadd_rn(s[j], r);
+      r = __dsub_rn(r, __dsub_rn(t, s[j]));
+      s[j] = t;
+    }
+    s[KE - 1] = __dadd_rn(s[KE - 1], r);
+  }
+#pragma unroll
+  for (int j = 0; j < KE; ++j) wb->s[j][ln] = s[j];
+}
+// this lane needs k bins -> the warp runs 2, 3, 4 or K (more than needed is
+// exact too: the extra bins take zeros; four forms, not K, keep the
+// fallback's code small), decided by votes (cheaper than a redux.max on the
+// path to the first DADD). k > K: not taken (returns false).
+template <int K, int GL>
+__device__ __forceinline__ bool bins_run_dispatch(WarpBins<K>* wb, const ExVals<GL>& xs, int k, unsigned mask,
+                                                  const double (&pre)[kBinPre]) {
+  static_assert(K >= 4, "K >= 4 bins");
+  if (!__any_sync(mask, k > 3)) {
+    if (__any_sync(mask, k > 2)) bins_run<K, 3, GL>(wb, xs, pre);
+    else bins_run<K, 2, GL>(wb, xs, pre);
+  } else if (!__any_sync(mask, k > 4)) {
+    bins_run<K, 4, GL>(wb, xs, pre);
+  } else {
+    if (__any_sync(mask, k > K)) return false;
+    bins_run<K, K, GL>(wb, xs, pre);
+  }
+  return true;
+}
+
+// One group of GL finite terms (gmax >= every floor(log2|x|), gmax <=
+// kBinMaxTop; glow <= the exponent of every nonzero term's lowest bit) into
+// this lane's bins; called from the out-of-line group fallbacks. fp64 terms
+// that reach below the K-th bin (exponents spread over more than ~300
+// binades in one warp's groups) are not taken (returns false: the caller's
+// per-element levels); fp32 terms always fit (K = 8 bins span the format).
 template <typename T, int K, int GL>
-__device__ __forceinline__ uint32_t bins_group(WarpBins<K>* wb, uint32_t flags, const ExVals<GL>& xs, int gmax,
-                                               int glow, long long* w) {
+__device__ __forceinline__ bool bins_group(WarpBins<K>* wb, uint32_t& flags, const ExVals<GL>& xs, int gmax,
+                                           int glow, long long* w) {
   const unsigned mask = __activemask();
-  Bins<K> bn = bins_load(wb);
-  if (gmax > bn.top || bn.count > kBinMaxAdds - GL) {   // re-anchor (per lane, rare)
+  const int ln = threadIdx.x & 31;
+  int top = wb->top[ln];
+  int count = wb->count[ln];
+  double pre[kBinPre];
+#pragma unroll
+  for (int j = 0; j < kBinPre; ++j) pre[j] = wb->s[j][ln];
+  if (gmax > top || count > kBinMaxAdds - GL) {      // re-anchor (per lane, rare)
+    Bins<K> bn = bins_load(wb);
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const double d = bin_value(bn, j);
       if (d != 0.0) sacc_add<T>(w, d);
     }
-    int a0 = bn.top + kBinHead;
-    if (gmax > bn.top) a0 = min(max(gmax + kBinHead + kBinSlack, bins_min_a0<K>()), 1023);
+    int a0 = top + kBinHead;
+    if (gmax > top) a0 = min(max(gmax + kBinHead + kBinSlack, bins_min_a0<K>()), 1023);
 #pragma unroll
     for (int j = 0; j < K; ++j) bn.s[j] = bin_anchor(a0 - j * kBinW);
-    bn.top = a0 - kBinHead;
-    bn.count = 0;
+    bn.top = top = a0 - kBinHead;
+    bn.count = count = 0;
+    bins_store(wb, bn);
+#pragma unroll
+    for (int j = 0; j < kBinPre; ++j) pre[j] = bn.s[j];
   }
   __syncwarp(mask);
-  bn.count += GL;
+  // the bins this lane needs: the fewest k whose last unit 2^(a_0 - (k-1)W -
+  // 52) is <= every term's lowest bit, k = 1 + ceil(span / W); the quotient
+  // by multiply-shift ((x * 1725) >> 16 == x / 38 for 0 <= x <= 2400; span <=
+  // 2046 for any double)
+  static_assert(kBinW == 38, "the multiply-shift divides by 38");
+  const int span = max(top + kBinHead - 52 - glow, 0);
+  const int k = 1 + (((span + kBinW - 1) * 1725) >> 16);
+  if (!bins_run_dispatch<K, GL>(wb, xs, k, mask, pre)) return false;   // (the re-anchoring kept the value)
+  wb->count[ln] = count + GL;
   bool nz = false;                                   // some term is not -0.0
 #pragma unroll
   for (int l = 0; l < GL; ++l) nz |= (uint64_t)__double_as_longlong(xs.v[l]) != kNegZeroBits;
   if (nz) flags |= kXNotNegZero;
-  const int low = bn.top + kBinHead - (K - 1) * kBinW - 52;   // exponent of the last bin's unit
-  if (__all_sync(mask, glow >= low)) {
-    // every term is a multiple of the last bin's unit: nothing falls below it
-#pragma unroll
-    for (int l = 0; l < GL; ++l) {
-      double r = xs.v[l];
-#pragma unroll
-      for (int j = 0; j < K - 1; ++j) {
-        const double t = __dadd_rn(bn.s[j], r);
-        r = __dsub_rn(r, __dsub_rn(t, bn.s[j]));
-        bn.s[j] = t;
-      }
-      bn.s[K - 1] = __dadd_rn(bn.s[K - 1], r);
-    }
-  } else {
-#pragma unroll
-    for (int l = 0; l < GL; ++l) {
-      double r = xs.v[l];
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const double t = __dadd_rn(bn.s[j], r);
-        r = __dsub_rn(r, __dsub_rn(t, bn.s[j]));
-        bn.s[j] = t;
-      }
-      if (r != 0.0) sacc_add<T>(w, r);
-    }
-  }
-  bins_store(wb, bn);
-  return flags;
+  return true;
 }
 
 // The per-element levels for a group whose group speculation failed, in
@@ -585,7 +624,8 @@ __device__ __noinline__ ExState<E, GL> exact32_fallback(ExState<E, GL> st, const
   }
   // floor(log2|x|) <= (mx >> 23) - 127; every nonzero term's lowest bit is at
   // least 2^((mn >> 23) - 150) (mn's field may be one below the term's)
-  st.flags = bins_group<float, K, GL>(wb, st.flags, xs, (int)(mx >> 23) - 127, (int)(mn >> 23) - 150, w);
+  static_assert(K >= 8, "fp32: the bins must span every exponent");   // 52 + 7 * 38 >= 277 + slack
+  bins_group<float, K, GL>(wb, st.flags, xs, (int)(mx >> 23) - 127, (int)(mn >> 23) - 150, w);
   return st;
 }
 
@@ -644,8 +684,9 @@ __device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], WarpBins<K>* wb,
 // fp64 data, one group the group path could not take, out of line (one
 // copy per kernel): the exponent fields are recomputed with the low words
 // (a subnormal below 2^-1042 has a zero high word but counts as exponent 0);
-// inf/NaN terms or a term past the bins' range (> 2^1007) in the warp -> the
-// per-element levels per 2 elements; else the bins.
+// inf/NaN terms or a term past the bins' range (> 2^1007) in the warp, or
+// terms that reach below the K-th bin -> the per-element levels per 2
+// elements; else the bins.
 template <int E, int GL, int K>
 __device__ __noinline__ ExState<E, GL> exact64_fallback(ExState<E, GL> st, const ExVals<GL> xs, WarpBins<K>* wb,
                                                         long long* w) {
@@ -656,13 +697,11 @@ __device__ __noinline__ ExState<E, GL> exact64_fallback(ExState<E, GL> st, const
     xmax = max(xmax, xh);
     xmin = min(xmin, xh - 1u);                       // zero -> 0xffffffff: no effect
   }
-  if (__any_sync(__activemask(), (xmax >> 20) > (uint32_t)(1023 + kBinMaxTop))) {
-    elementwise_pieces<double, E, GL, 2>(st, xs, w);
-    return st;
-  }
   // floor(log2|x|) <= (xmax >> 20) - 1023; every nonzero term's lowest bit is
   // at least 2^((xmin >> 20) - 1075)
-  st.flags = bins_group<double, K, GL>(wb, st.flags, xs, (int)(xmax >> 20) - 1023, (int)(xmin >> 20) - 1075, w);
+  if (__any_sync(__activemask(), (xmax >> 20) > (uint32_t)(1023 + kBinMaxTop)) ||
+      !bins_group<double, K, GL>(wb, st.flags, xs, (int)(xmax >> 20) - 1023, (int)(xmin >> 20) - 1075, w))
+    elementwise_pieces<double, E, GL, 2>(st, xs, w);
   return st;
 }
 
@@ -1030,7 +1069,6 @@ __device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], const WarpBins<K>* 
     dv[3 * j + 1] = ex[j].a1;
     dv[3 * j + 2] = ex[j].a2;
   }
-#pragma unroll
   {
     const Bins<K> bn = bins_load(&wbins[warp]);
 #pragma unroll
@@ -1285,6 +1323,14 @@ __global__ void __launch_bounds__(B, MINB) rd_exact_cluster_kernel(const __grid_
 // slice of each stage into fold_vec_exact. Memory parallelism comes from the
 // ring (STAGES * STAGE_BYTES in flight per SM), not from registers -- the
 // vector kernel's 118 registers/thread cap it at 16 warps/SM.
+// the exact bulk kernel's dynamic shared memory: the ring, its barriers and
+// stage metadata (BulkSmem), then one WarpBins block per warp
+template <typename T, int STAGES, int STAGE_BYTES, int CW>
+struct ExactBulkSmem {
+  static constexpr int kBins = BulkSmem<STAGES, STAGE_BYTES, CW>::kBytes;
+  static constexpr int kBytes = kBins + (CW + 1) * (int)sizeof(WarpBins<BinK<T>::K>);
+};
+
 template <typename T, int STAGES, int STAGE_BYTES, int CW, int E>
 __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const __grid_constant__ XArgs args) {
   using TR = ExactTraits<T>;
@@ -1300,7 +1346,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) rd_exact_bulk_kernel(const _
   uint64_t* empty = full + STAGES;
   uint32_t* st_bytes = reinterpret_cast<uint32_t*>(empty + STAGES);   // 0 = no more chunks
   __shared__ long long sacc[B / 32][NW];
-  __shared__ WarpBins<BinK<T>::K> wbins[B / 32];
+  WarpBins<BinK<T>::K>* wbins =                      // dynamic: past the 48 KB static limit
+      reinterpret_cast<WarpBins<BinK<T>::K>*>(smem_raw + ExactBulkSmem<T, STAGES, STAGE_BYTES, CW>::kBins);
   __shared__ long long tot[B];
   __shared__ unsigned s_flags, s_last;
 

@@ -30,7 +30,7 @@ static bool pick(int u, int e, int m, ExactRef* r) {
 template <typename T, int CW, int E, int STAGES = kBulkStages, int SB = kBulkStageBytes>
 static bool bulk_ref(ExactRef* r) {
   *r = ExactRef{rd_exact_bulk_kernel<T, STAGES, SB, CW, E>, 32 * (CW + 1), STAGES, SB, RD_VARIANT_BULK,
-                BulkSmem<STAGES, SB, CW>::kBytes};
+                ExactBulkSmem<T, STAGES, SB, CW>::kBytes};
   return true;
 }
 
