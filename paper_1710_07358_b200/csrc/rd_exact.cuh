@@ -13,9 +13,13 @@
 //      vector it SPECULATES branch-free -- fp32 data: every add into a0 is
 //      exact, tested by compares only (fl(s - a0) == x && fl(s - x) == a0;
 //      3 DADD + 2 compares per element); fp64 data: a0's TwoSum error goes into
-//      a1 exactly -- with ONE branch per vector. A failed vector is replayed
-//      element by element out of line (replay_vec: a0 -> a1 -> a2 TwoSums;
-//      only a nonzero third error, an fp64 overflow or inf/NaN reaches the
+//      a1 exactly -- with ONE branch per vector; the streaming loops do the
+//      same per GROUP of 8 terms with one tested add (fold_group_exact32/64).
+//      A group they cannot take goes out of line to the BINS (binned
+//      extraction into 8 fixed-exponent fp64 bins per lane, exact by its
+//      invariants, bins_group); inf/NaN terms and fp64 spreads past the bins
+//      go element by element (replay_vec: a0 -> a1 -> a2 TwoSums; only a
+//      nonzero third error, an fp64 overflow or inf/NaN reaches the
 //      superaccumulator). Loops end with __syncwarp so replays reconverge.
 //  superaccumulator: a fixed-point integer whose unit is the dtype's smallest
 //      subnormal (2^-149 / 2^-1074), held as kWords carry-save int64 words of
@@ -120,6 +124,25 @@ __device__ __forceinline__ void sacc_add(long long* w, double d) {
   const long long d0 = (long long)(lo & 0xffffffffull), d1 = (long long)(lo >> 32);
   const long long d2 = r ? (long long)(m >> (64 - r)) : 0;
   const bool neg = (int64_t)b < 0;
+  if (d0) sacc_word_add<TR::kWords>(w, k, neg ? -d0 : d0);
+  if (d1) sacc_word_add<TR::kWords>(w, k + 1, neg ? -d1 : d1);
+  if (d2) sacc_word_add<TR::kWords>(w, k + 2, neg ? -d2 : d2);
+}
+
+// deposit the signed integer v (|v| < 2^62) times 2^e exactly, e an exponent
+// at or above the dtype's smallest unit whenever v has bits below it (the
+// bins' contents are sums of terms, so multiples of 2^kLsb)
+template <typename T>
+__device__ __forceinline__ void sacc_add_units(long long* w, long long v, int e) {
+  using TR = ExactTraits<T>;
+  const bool neg = v < 0;
+  uint64_t m = neg ? (uint64_t)(-v) : (uint64_t)v;
+  int p = e - TR::kLsb;              // bit position of v's unit
+  if (p < 0) { m >>= -p; p = 0; }    // only zero bits
+  const int k = p >> 5, r = p & 31;
+  const uint64_t lo = m << r;
+  const long long d0 = (long long)(lo & 0xffffffffull), d1 = (long long)(lo >> 32);
+  const long long d2 = r ? (long long)(m >> (64 - r)) : 0;
   if (d0) sacc_word_add<TR::kWords>(w, k, neg ? -d0 : d0);
   if (d1) sacc_word_add<TR::kWords>(w, k + 1, neg ? -d1 : d1);
   if (d2) sacc_word_add<TR::kWords>(w, k + 2, neg ? -d2 : d2);
@@ -408,6 +431,79 @@ __device__ __forceinline__ void fold_vec_exact(Ex (&ex)[E], const double (&xs)[L
   }
 }
 
+// The end-of-thread deposit, warp-cooperative, in registers and without
+// atomics: every lane of the (converged) warp passes its NV doubles (0 =
+// nothing). The warp walks the superaccumulator words its lanes' digits land
+// in (the next occupied word comes from one redux.min); per word each lane
+// sums its own digits there (|c| < 2^35), the warp adds the 32 lane sums with
+// three 13-bit-chunk redux.sync adds (offset to be nonnegative: no chunk sum
+// overflows), and lane 0 adds the total to the word. (Per-lane shared 64-bit
+// atomics are CAS loops on sm_100a, ATOMS.CAST.SPIN.64, and a smem-staged
+// transposed sum costs ~2000 instructions per warp: both dominated small n.)
+// Only this warp writes its superaccumulator, and its slow-path atomics are
+// complete (__syncwarp). `mask`: the lanes taking part (all of them converged
+// here; the lowest adds the word sums).
+template <typename T, int NV>
+__device__ __forceinline__ void sacc_flush_warp(long long* w, const double (&d)[NV], unsigned mask = 0xffffffffu) {
+  using TR = ExactTraits<T>;
+  constexpr int kNone = 0x7fffffff;
+  int k[NV];
+  long long s0[NV], s1[NV], s2[NV];
+  int first = kNone;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    k[v] = kNone;
+    s0[v] = s1[v] = s2[v] = 0;
+    if (d[v] != 0.0) {
+      const uint64_t b = (uint64_t)__double_as_longlong(d[v]);
+      int e = (int)((b >> 52) & 0x7ff);
+      uint64_t m = b & ((1ull << 52) - 1);
+      if (e) m |= 1ull << 52;
+      else e = 1;
+      int p = e - 1075 - TR::kLsb;
+      if (p < 0) { m >>= -p; p = 0; }
+      const int r = p & 31;
+      const uint64_t lo = m << r;
+      s0[v] = (long long)(lo & 0xffffffffull);
+      s1[v] = (long long)(lo >> 32);
+      s2[v] = r ? (long long)(m >> (64 - r)) : 0;
+      if ((int64_t)b < 0) { s0[v] = -s0[v]; s1[v] = -s1[v]; s2[v] = -s2[v]; }
+      k[v] = p >> 5;
+      first = min(first, k[v]);
+    }
+  }
+  const bool writer = (int)(threadIdx.x & 31) == __ffs(mask) - 1;
+  const long long offset = (long long)__popc(mask) << 38;
+  int word = __reduce_min_sync(mask, first);
+  while (word != kNone) {                            // warp-uniform
+    long long c = 0;
+    int next = kNone;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      c += (k[v] == word ? s0[v] : 0) + (k[v] + 1 == word ? s1[v] : 0) + (k[v] + 2 == word ? s2[v] : 0);
+      // this lane's next occupied word above `word` (k, k+1, k+2 of each value)
+      if (k[v] != kNone) {
+        const int d0 = k[v] - word;                  // in [-2, inf)
+        const int cand = d0 > 0 ? k[v] : (d0 > -2 ? k[v] + 2 - (d0 == 0 ? 1 : 0) : kNone);
+        next = min(next, cand);
+      }
+    }
+    const unsigned long long u = (unsigned long long)(c + (1ll << 38));   // in [0, 2^39)
+    const unsigned c0 = __reduce_add_sync(mask, (unsigned)(u & 0x1fff));
+    const unsigned c1 = __reduce_add_sync(mask, (unsigned)((u >> 13) & 0x1fff));
+    const unsigned c2 = __reduce_add_sync(mask, (unsigned)(u >> 26));
+    if (writer) {
+      const long long v = (long long)c0 + ((long long)c1 << 13) + ((long long)c2 << 26) - offset;
+      // a partial warp (a tail loop): the lanes outside it may be depositing
+      // stragglers into the same words by atomics meanwhile
+      if (mask == 0xffffffffu) w[word] += v;
+      else atomicAdd((unsigned long long*)&w[word], (unsigned long long)v);
+    }
+    word = __reduce_min_sync(mask, next);
+  }
+  __syncwarp(mask);
+}
+
 // ------------------------------------------------------------------- bins
 // The fallback for groups the group paths cannot sum exactly (exponents
 // spread wider than one fp64 significand can hold: the `wide` workload, where
@@ -559,22 +655,40 @@ __device__ __forceinline__ bool bins_group(WarpBins<K>* wb, uint32_t& flags, con
   double pre[kBinPre];
 #pragma unroll
   for (int j = 0; j < kBinPre; ++j) pre[j] = wb->s[j][ln];
-  if (gmax > top || count > kBinMaxAdds - GL) {      // re-anchor (per lane, rare)
-    Bins<K> bn = bins_load(wb);
+  if (__any_sync(mask, gmax > top || count > kBinMaxAdds - GL)) {
+    // re-anchor, the whole warp at once (rare). The anchor is the same in
+    // every lane of a warp, so the warp re-anchors when ITS maximum grows (a
+    // few times per launch, not once per lane), and bin j holds a multiple of
+    // the same unit u_j in every lane: its content in units, m = bits(S_j) -
+    // bits(1.5 * 2^a_j) (same binade: the difference of the bit patterns;
+    // |m| < 2^50), is summed over the warp exactly by three 17-bit-chunk
+    // redux adds, and ONE lane deposits the total (< 2^55 units) -- per-lane
+    // atomic deposits were CAS loops contended by 32 lanes on the same words
+    // (~40 us per launch at 2^24). The bins then start empty, re-anchored
+    // higher if the warp's maximum grew.
+    const int a0 = top + kBinHead;
+    const bool writer = (int)ln == __ffs(mask) - 1;
+    const long long off = (long long)__popc(mask) << 50;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      const double d = bin_value(bn, j);
-      if (d != 0.0) sacc_add<T>(w, d);
+      const long long m = __double_as_longlong(wb->s[j][ln]) - __double_as_longlong(bin_anchor(a0 - j * kBinW));
+      const unsigned long long u = (unsigned long long)(m + (1ll << 50));          // [0, 2^51)
+      const long long tot = (long long)__reduce_add_sync(mask, (unsigned)(u & 0x1ffffu)) +
+                            ((long long)__reduce_add_sync(mask, (unsigned)((u >> 17) & 0x1ffffu)) << 17) +
+                            ((long long)__reduce_add_sync(mask, (unsigned)(u >> 34)) << 34) - off;
+      if (writer && tot != 0) sacc_add_units<T>(w, tot, a0 - j * kBinW - 52);
     }
-    int a0 = top + kBinHead;
-    if (gmax > top) a0 = min(max(gmax + kBinHead + kBinSlack, bins_min_a0<K>()), 1023);
+    const int wmax = __reduce_max_sync(mask, gmax);
+    const int na0 = wmax > top ? min(max(wmax + kBinHead + kBinSlack, bins_min_a0<K>()), 1023) : a0;
 #pragma unroll
-    for (int j = 0; j < K; ++j) bn.s[j] = bin_anchor(a0 - j * kBinW);
-    bn.top = top = a0 - kBinHead;
-    bn.count = count = 0;
-    bins_store(wb, bn);
-#pragma unroll
-    for (int j = 0; j < kBinPre; ++j) pre[j] = bn.s[j];
+    for (int j = 0; j < K; ++j) {
+      const double sj = bin_anchor(na0 - j * kBinW);
+      wb->s[j][ln] = sj;
+      if (j < kBinPre) pre[j < kBinPre ? j : 0] = sj;
+    }
+    top = na0 - kBinHead;
+    wb->top[ln] = top;
+    count = 0;
   }
   __syncwarp(mask);
   // the bins this lane needs: the fewest k whose last unit 2^(a_0 - (k-1)W -
@@ -980,71 +1094,6 @@ __device__ __noinline__ void exact_fused_exchange(long long* words, unsigned fla
   }
 }
 
-// The end-of-thread deposit, warp-cooperative, in registers and without
-// atomics: every lane of the (converged) warp passes its NV doubles (0 =
-// nothing). The warp walks the superaccumulator words its lanes' digits land
-// in (the next occupied word comes from one redux.min); per word each lane
-// sums its own digits there (|c| < 2^35), the warp adds the 32 lane sums with
-// three 13-bit-chunk redux.sync adds (offset to be nonnegative: no chunk sum
-// overflows), and lane 0 adds the total to the word. (Per-lane shared 64-bit
-// atomics are CAS loops on sm_100a, ATOMS.CAST.SPIN.64, and a smem-staged
-// transposed sum costs ~2000 instructions per warp: both dominated small n.)
-// Only this warp writes its superaccumulator, and its slow-path atomics are
-// complete (__syncwarp).
-template <typename T, int NV>
-__device__ __forceinline__ void sacc_flush_warp(long long* w, const double (&d)[NV]) {
-  using TR = ExactTraits<T>;
-  constexpr int kNone = 0x7fffffff;
-  int k[NV];
-  long long s0[NV], s1[NV], s2[NV];
-  int first = kNone;
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    k[v] = kNone;
-    s0[v] = s1[v] = s2[v] = 0;
-    if (d[v] != 0.0) {
-      const uint64_t b = (uint64_t)__double_as_longlong(d[v]);
-      int e = (int)((b >> 52) & 0x7ff);
-      uint64_t m = b & ((1ull << 52) - 1);
-      if (e) m |= 1ull << 52;
-      else e = 1;
-      int p = e - 1075 - TR::kLsb;
-      if (p < 0) { m >>= -p; p = 0; }
-      const int r = p & 31;
-      const uint64_t lo = m << r;
-      s0[v] = (long long)(lo & 0xffffffffull);
-      s1[v] = (long long)(lo >> 32);
-      s2[v] = r ? (long long)(m >> (64 - r)) : 0;
-      if ((int64_t)b < 0) { s0[v] = -s0[v]; s1[v] = -s1[v]; s2[v] = -s2[v]; }
-      k[v] = p >> 5;
-      first = min(first, k[v]);
-    }
-  }
-  int word = __reduce_min_sync(0xffffffffu, first);
-  while (word != kNone) {                            // warp-uniform
-    long long c = 0;
-    int next = kNone;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      c += (k[v] == word ? s0[v] : 0) + (k[v] + 1 == word ? s1[v] : 0) + (k[v] + 2 == word ? s2[v] : 0);
-      // this lane's next occupied word above `word` (k, k+1, k+2 of each value)
-      if (k[v] != kNone) {
-        const int d0 = k[v] - word;                  // in [-2, inf)
-        const int cand = d0 > 0 ? k[v] : (d0 > -2 ? k[v] + 2 - (d0 == 0 ? 1 : 0) : kNone);
-        next = min(next, cand);
-      }
-    }
-    const unsigned long long u = (unsigned long long)(c + (1ll << 38));   // in [0, 2^39)
-    const unsigned c0 = __reduce_add_sync(0xffffffffu, (unsigned)(u & 0x1fff));
-    const unsigned c1 = __reduce_add_sync(0xffffffffu, (unsigned)((u >> 13) & 0x1fff));
-    const unsigned c2 = __reduce_add_sync(0xffffffffu, (unsigned)(u >> 26));
-    if ((threadIdx.x & 31) == 0)
-      w[word] += (long long)c0 + ((long long)c1 << 13) + ((long long)c2 << 26) - (32ll << 38);
-    word = __reduce_min_sync(0xffffffffu, next);
-  }
-  __syncwarp();
-}
-
 // a3-a5, shared by the exact kernels: the expansions -> warp
 // superaccumulators -> the CTA's carried-digit sums in cta[0..NW) (< 2^35 per
 // word) and its flags in cta[NW]. Ends with __syncthreads.
@@ -1061,7 +1110,7 @@ __device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], const WarpBins<K>* 
   // has seen a term other than -0.0 is never -0.0 again (x + -x = +0), so a0
   // alone decides reading R2's "every term is -0.0".
   __syncwarp();
-  double dv[3 * E + K];
+  double dv[3 * E];
 #pragma unroll
   for (int j = 0; j < E; ++j) {
     if ((uint64_t)__double_as_longlong(ex[j].a0) != kNegZeroBits) flags |= kXNotNegZero;
@@ -1069,12 +1118,17 @@ __device__ __forceinline__ void exact_cta_words(Ex (&ex)[E], const WarpBins<K>* 
     dv[3 * j + 1] = ex[j].a1;
     dv[3 * j + 2] = ex[j].a2;
   }
-  {
+  sacc_flush_warp<T, 3 * E>(w, dv);
+  // the bins' contents (flags set by bins_group), only if some lane of the warp
+  // added to its bins since the last re-anchoring (count > 0): most data never
+  // reaches them, and small launches are epilogue-bound
+  if (__any_sync(0xffffffffu, wbins[warp].count[ln] > 0)) {
     const Bins<K> bn = bins_load(&wbins[warp]);
+    double bv[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) dv[3 * E + j] = bin_value(bn, j);   // the bins' contents (flags set by bins_group)
+    for (int j = 0; j < K; ++j) bv[j] = bin_value(bn, j);
+    sacc_flush_warp<T, K>(w, bv);
   }
-  sacc_flush_warp<T, 3 * E + K>(w, dv);
   flags = __reduce_or_sync(0xffffffffu, flags);
   if (ln == 0 && flags) atomicOr(&s_flags, flags);
   __syncwarp();

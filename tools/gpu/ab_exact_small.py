@@ -21,4 +21,4 @@ for log2n in (14, 16, 18):
         a.record(); g.replay(); b.record(); b.synchronize()
         ts.append(a.elapsed_time(b) * 10.0)
     res[f"2^{log2n}"] = round(sorted(ts)[3], 3)
-print(json.dumps({"lib": os.path.basename(sys.argv[1]), **res}))
+print(json.dumps({"lib": os.path.relpath(sys.argv[1]), "dt": DT, **res}))
