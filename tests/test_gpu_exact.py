@@ -337,3 +337,27 @@ def test_exact_fp64_subnormal_high_word_zero(rd):
     xd = to_dev(x, 1)
     for variant in ("auto", "vector", "bulk"):
         assert same(val(rd.reduce_ex(xd, "sum_exact", variant=variant)[0]), want), variant
+
+
+@pytest.mark.parametrize("dtype", FLT)
+def test_exact_bins_at_scale(rd, dtype):
+    """2^31 `wide` terms (8 / 16 GiB): ~28k terms per thread on the bulk kernel, so
+    every warp re-anchors on its addition limit several times, with different
+    thread-to-term assignments per form -- the whole array, 8 shard records, a
+    forced grid and the vector form must give the same bits (reading R17)."""
+    n = 1 << 31
+    free, _ = torch.cuda.mem_get_info()
+    if free < n * np.dtype(dtype).itemsize + (8 << 30):
+        pytest.skip("needs the array plus 8 GiB of free HBM")
+    x = torch.empty(n, dtype=getattr(torch, dtype), device="cuda")
+    inputs.fill_device(x, "wide", seed=2)
+    RB = rd.EXACT_RECORD_BYTES
+    recs = torch.empty(8 * RB, dtype=torch.uint8, device="cuda")
+    for r in range(8):
+        b, c = rd.shard_range(n, 8, r)
+        rd.reduce_exact_partial(x[b:b + c], rec=recs[r * RB:(r + 1) * RB])
+    got = {bits(val(rd.reduce(x, "sum_exact"))), bits(val(rd.combine_exact_records(recs, dtype))),
+           bits(val(rd.reduce_ex(x, "sum_exact", grid=777)[0])),
+           bits(val(rd.reduce_ex(x, "sum_exact", variant="vector")[0]))}
+    del x
+    assert len(got) == 1
