@@ -647,7 +647,7 @@ __device__ __forceinline__ bool bins_run_dispatch(WarpBins<K>* wb, const ExVals<
 // per-element levels); fp32 terms always fit (K = 8 bins span the format).
 template <typename T, int K, int GL>
 __device__ __forceinline__ bool bins_group(WarpBins<K>* wb, uint32_t& flags, const ExVals<GL>& xs, int gmax,
-                                           int glow, long long* w) {
+                                           int glow, bool nonzero, long long* w) {
   const unsigned mask = __activemask();
   const int ln = threadIdx.x & 31;
   int top = wb->top[ln];
@@ -700,9 +700,12 @@ __device__ __forceinline__ bool bins_group(WarpBins<K>* wb, uint32_t& flags, con
   const int k = 1 + (((span + kBinW - 1) * 1725) >> 16);
   if (!bins_run_dispatch<K, GL>(wb, xs, k, mask, pre)) return false;   // (the re-anchoring kept the value)
   wb->count[ln] = count + GL;
-  bool nz = false;                                   // some term is not -0.0
+  // "some term is not -0.0": a nonzero term (the caller's max |bits| != 0), or a +0.0
+  bool nz = nonzero;
+  if (!nz) {
 #pragma unroll
-  for (int l = 0; l < GL; ++l) nz |= (uint64_t)__double_as_longlong(xs.v[l]) != kNegZeroBits;
+    for (int l = 0; l < GL; ++l) nz |= (uint64_t)__double_as_longlong(xs.v[l]) != kNegZeroBits;
+  }
   if (nz) flags |= kXNotNegZero;
   return true;
 }
@@ -725,22 +728,24 @@ __device__ __forceinline__ void elementwise_pieces(ExState<E, GL>& st, const ExV
 }
 
 // fp32 data, one group the group path could not take, out of line (one
-// copy per kernel, one cold call site per group): inf/NaN terms in the warp
-// -> fold_vec_exact's per-element levels (tested adds into a0, two TwoSum
-// levels, the element replay) per 4 elements, which keep the flags; else the
-// bins. mx / mn: the group's max |bits| and min |bits| - 1 (zeros skipped).
-template <int E, int GL, int K>
-__device__ __noinline__ ExState<E, GL> exact32_fallback(ExState<E, GL> st, const ExVals<GL> xs, WarpBins<K>* wb,
-                                                        uint32_t mx, uint32_t mn, long long* w) {
-  if (__any_sync(__activemask(), mx >= 0x7f800000u)) {
-    elementwise_pieces<float, E, GL, (GL < 4 ? GL : 4)>(st, xs, w);
-    return st;
-  }
+// copy per kernel): inf/NaN terms in the warp -> fold_vec_exact's
+// per-element levels (tested adds into a0, two TwoSum levels, the element
+// replay) per 4 elements, which keep the flags (exact32_special); else the
+// bins (exact32_bins: no expansion state crosses the call). mx / mn: the
+// group's max |bits| and min |bits| - 1 (zeros skipped).
+template <int E, int GL>
+__device__ __noinline__ ExState<E, GL> exact32_special(ExState<E, GL> st, const ExVals<GL> xs, long long* w) {
+  elementwise_pieces<float, E, GL, (GL < 4 ? GL : 4)>(st, xs, w);
+  return st;
+}
+template <int GL, int K>
+__device__ __noinline__ uint32_t exact32_bins(uint32_t flags, const ExVals<GL> xs, WarpBins<K>* wb, uint32_t mx,
+                                              uint32_t mn, long long* w) {
   // floor(log2|x|) <= (mx >> 23) - 127; every nonzero term's lowest bit is at
   // least 2^((mn >> 23) - 150) (mn's field may be one below the term's)
   static_assert(K >= 8, "fp32: the bins must span every exponent");   // 52 + 7 * 38 >= 277 + slack
-  bins_group<float, K, GL>(wb, st.flags, xs, (int)(mx >> 23) - 127, (int)(mn >> 23) - 150, w);
-  return st;
+  bins_group<float, K, GL>(wb, flags, xs, (int)(mx >> 23) - 127, (int)(mn >> 23) - 150, mx != 0, w);
+  return flags;
 }
 
 // fp32 data, a GROUP of GL elements (one LDG.256, or two LDS.128 of the bulk
@@ -782,17 +787,21 @@ __device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], WarpBins<K>* wb,
     q.a0 = t;
     return;
   }
-  ExState<E, GL> st;
-#pragma unroll
-  for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
-  st.flags = flags;
   ExVals<GL> v;
 #pragma unroll
   for (int l = 0; l < GL; ++l) v.v[l] = x[l];
-  st = exact32_fallback<E, GL, K>(st, v, wb, mx, mn, w);
+  if (__any_sync(mask, special)) {
+    ExState<E, GL> st;
 #pragma unroll
-  for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
-  flags = st.flags;
+    for (int j = 0; j < E; ++j) st.ex[j] = ex[j];
+    st.flags = flags;
+    st = exact32_special<E, GL>(st, v, w);
+#pragma unroll
+    for (int j = 0; j < E; ++j) ex[j] = st.ex[j];
+    flags = st.flags;
+  } else {
+    flags = exact32_bins<GL, K>(flags, v, wb, mx, mn, w);
+  }
 }
 
 // fp64 data, one group the group path could not take, out of line (one
@@ -814,7 +823,8 @@ __device__ __noinline__ ExState<E, GL> exact64_fallback(ExState<E, GL> st, const
   // floor(log2|x|) <= (xmax >> 20) - 1023; every nonzero term's lowest bit is
   // at least 2^((xmin >> 20) - 1075)
   if (__any_sync(__activemask(), (xmax >> 20) > (uint32_t)(1023 + kBinMaxTop)) ||
-      !bins_group<double, K, GL>(wb, st.flags, xs, (int)(xmax >> 20) - 1023, (int)(xmin >> 20) - 1075, w))
+      !bins_group<double, K, GL>(wb, st.flags, xs, (int)(xmax >> 20) - 1023, (int)(xmin >> 20) - 1075, xmax != 0,
+                                 w))
     elementwise_pieces<double, E, GL, 2>(st, xs, w);
   return st;
 }
