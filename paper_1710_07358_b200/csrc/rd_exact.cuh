@@ -779,13 +779,15 @@ __device__ __forceinline__ void fold_group_exact32(Ex (&ex)[E], WarpBins<K>* wb,
   }
   const bool special = mx >= 0x7f800000u;
   const bool wide = (int)(mx >> 23) - (int)(mn >> 23) > kMaxSpread;
-  const double s = tree_sum<GL>(x);                  // exact when the spread test holds
-  Ex& q = ex[g % E];
-  const double t = __dadd_rn(q.a0, s);
-  const bool bad = special | wide | (__dsub_rn(t, q.a0) != s) | (__dsub_rn(t, s) != q.a0);
-  if (__builtin_expect(!__any_sync(mask, bad), 1)) {
-    q.a0 = t;
-    return;
+  if (__builtin_expect(!__any_sync(mask, special | wide), 1)) {   // (no group work thrown away on wide data)
+    const double s = tree_sum<GL>(x);                // exact: the spread test holds
+    Ex& q = ex[g % E];
+    const double t = __dadd_rn(q.a0, s);
+    const bool bad = (__dsub_rn(t, q.a0) != s) | (__dsub_rn(t, s) != q.a0);
+    if (__builtin_expect(!__any_sync(mask, bad), 1)) {
+      q.a0 = t;
+      return;
+    }
   }
   ExVals<GL> v;
 #pragma unroll
