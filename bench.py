@@ -492,6 +492,19 @@ def run_b200(args):
                                 "workload": "uniform_bits, seed 1", "check_bit_exact": bool(got == want),
                                 "cub_device_reduce_gbs": cub_gbs(xi, 0, 0) if cub is not None else None}
             del xi
+            # the exact sum on its adversarial workload (exponents over 2^+-40: nearly
+            # every group takes the binned-extraction fallback), same n,
+            # checked bit-exact against the oracle's exact sum
+            import numpy as np
+            xw = torch.empty(n, dtype=torch.float32, device=dev)
+            inputs.fill_device(xw, "wide", seed=1)
+            ow = torch.empty((), dtype=torch.float32, device=dev)
+            ms = time_b2b(lambda: rd.reduce(xw, "sum_exact", out=ow), R, stream)
+            got = to_np(ow)
+            want = oracle.reduce(xw.cpu().numpy(), "sum_exact").value
+            ctx["sum_exact_wide"] = {"gbs": round(gbps(n * 4, ms / 1e3), 2), "n": n, "workload": "wide, seed 1",
+                                     "check_bit_exact": bool(np.asarray(got).tobytes() == np.asarray(want).tobytes())}
+            del xw
 
         # the same-run HBM read ceiling (SURVEY §8(d) peak 3): the read probe
         # (tools/probe.cu: 256-bit loads xor-folded, no reduction semantics) over

@@ -100,6 +100,10 @@ typedef enum {
    * rd_combine_exact_records (the 32-byte rd_record cannot carry an exact
    * partial, so reduce_partial and rd_combine_records return
    * RD_ERR_UNSUPPORTED for float dtypes).
+   * Throughput depends on the data, never the result: near the plain sum's
+   * when the terms' exponents cluster (uniform / normal data), about half of
+   * it when they spread over ~80 binades (binned extraction),
+   * lowest for fp64 terms spread over hundreds of binades.
    * Integers: identical to RD_SUM everywhere. */
   RD_SUM_EXACT = 10
 } rd_op;

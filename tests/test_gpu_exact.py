@@ -305,6 +305,16 @@ def test_exact_bins(rd, dtype):
         xd = to_dev(x, 3)
         for variant in ("auto", "vector", "bulk"):
             assert same(val(rd.reduce_ex(xd, "sum_exact", variant=variant)[0]), want), (dtype, variant)
+    # specials among groups that take the bins: the warp holding them goes per
+    # element, every other warp stays in the bins
+    base = inputs.generate((1 << 20) + 3, dtype, "wide", seed=6)
+    for specials in ([np.inf], [-np.inf], [np.nan], [np.inf, -np.inf], [-0.0, np.inf]):
+        y = base.copy()
+        y[rng.integers(0, y.size, len(specials))] = specials
+        want = oracle.reduce(y, "sum_exact").value
+        yd = to_dev(y, 1)
+        for variant in ("auto", "vector", "bulk"):
+            assert same(val(rd.reduce_ex(yd, "sum_exact", variant=variant)[0]), want), (dtype, specials, variant)
     # long per-thread runs: one CTA over 2^22 wide terms -> > 4096 additions per bin
     x = inputs.generate(1 << 22, dtype, "wide", seed=8)
     want = oracle.reduce(x, "sum_exact").value
