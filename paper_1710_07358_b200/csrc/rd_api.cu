@@ -465,8 +465,13 @@ rd_status launch_exact(const void* x, size_t n, int dtype, int mode, void* out, 
     return RD_ERR_INVALID_ARG;
   }
   if (variant == RD_VARIANT_AUTO) {
+    // fp64 terms: the bulk ring above the one-cluster range (the vector form's
+    // 128-register threads trail it at every size from 2 MiB, cold and
+    // graph-captured: 2^22 20.5 vs 27.7 us; profiles/r02_exact_variants.json);
+    // fp32 terms: the vector form below 128 MiB (ahead graph-captured at 4-64 MiB)
     const uint64_t bytes = (uint64_t)n * s;
-    variant = bytes >= kBulkMinBytes ? RD_VARIANT_BULK
+    const uint64_t bulk_from = dtype == RD_FLOAT64 ? kClusterMaxBytes + 1 : kBulkMinBytes;
+    variant = bytes >= bulk_from ? RD_VARIANT_BULK
               : (bytes > (uint64_t)kBlock * kExactUnroll * 32 && bytes <= kClusterMaxBytes &&
                  !(cfg && cfg->grid > kClusterMax)) ? RD_VARIANT_CLUSTER : RD_VARIANT_VECTOR;
   }

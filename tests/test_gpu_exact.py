@@ -371,3 +371,19 @@ def test_exact_bins_at_scale(rd, dtype):
            bits(val(rd.reduce_ex(x, "sum_exact", variant="vector")[0]))}
     del x
     assert len(got) == 1
+
+
+def test_exact_auto_plan(rd):
+    """The exact sum's AUTO variant (rd_api.cu, profiles/r02_exact_variants.json): the
+    one-cluster form up to 1 MiB; above it fp64 terms take the bulk ring at every size,
+    fp32 terms the vector form below 128 MiB and the bulk ring from there."""
+    def plan(dtype, nbytes):
+        x = torch.zeros(nbytes // np.dtype(dtype).itemsize, dtype=getattr(torch, dtype), device="cuda")
+        return rd.reduce_ex(x, "sum_exact")[1]["variant"]
+
+    for dtype in FLT:
+        assert plan(dtype, 512 << 10) == "cluster"
+        assert plan(dtype, 1 << 20) == "cluster"
+        assert plan(dtype, 128 << 20) == "bulk"
+    assert plan("float64", 2 << 20) == "bulk" and plan("float64", 64 << 20) == "bulk"
+    assert plan("float32", 2 << 20) == "vector" and plan("float32", 64 << 20) == "vector"

@@ -293,6 +293,33 @@ def do_midops(args):
     return rows
 
 
+def do_exactvariants(args):
+    """The exact sum's variants at mid sizes (2^18..2^27), per dtype and workload:
+    vector vs bulk (and the one-cluster form where it applies), cold single launch
+    (L2 flushed) and graph-captured back to back -- the basis of the exact sum's
+    AUTO threshold."""
+    rows = []
+    for dtype in ("float32", "float64"):
+        for wl in ("u01", "wide"):
+            for log2n in range(18, 28):
+                n = 1 << log2n
+                x = make(n, dtype, wl)
+                o = torch.empty((), dtype=x.dtype, device="cuda")
+                _, info = rd.reduce_ex(x, "sum_exact", out=o)
+                for variant in ("vector", "bulk", "cluster"):
+                    if variant == "cluster" and n * x.element_size() > (1 << 20):
+                        continue
+                    fn = lambda: rd.reduce_ex(x, "sum_exact", variant=variant, out=o)
+                    cold = time_launch(fn, n * x.element_size(), reps=20)
+                    r = {"dtype": dtype, "workload": wl, "n": n, "log2n": log2n, "variant": variant,
+                         "auto_variant": info["variant"], "cold_us": round(cold["t_med_us"], 2),
+                         "graph_us": graph_us(fn)}
+                    rows.append(r)
+                    print(json.dumps(r), flush=True)
+                del x
+    return rows
+
+
 def do_grids(args):
     """Grid multiplier (waves of resident CTAs) for the default kernels at n = 2^28."""
     rows = []
@@ -491,14 +518,14 @@ def do_context(args):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi", "overhead",
-                                    "exact", "midgrids", "midops", "context"])
+                                    "exact", "midgrids", "midops", "context", "exactvariants"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
     args = p.parse_args()
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
            "grids": do_grids, "crossover": do_crossover, "multi": do_multi,
-           "overhead": do_overhead, "exact": do_exact,
+           "overhead": do_overhead, "exact": do_exact, "exactvariants": do_exactvariants,
            "midgrids": do_midgrids, "midops": do_midops, "context": do_context}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
