@@ -288,7 +288,12 @@ rd_status launch_reduce(const void* x, size_t n, int dtype, int op, int mode, vo
   if (vec_bytes && vec_bytes < s && variant != RD_VARIANT_BULK) { set_error("vec_bytes < sizeof(dtype)"); return RD_ERR_INVALID_ARG; }
   if (variant == RD_VARIANT_AUTO && unroll == 0 && vec_bytes == 0) {
     const uint64_t bytes = (uint64_t)n * s;
-    if (bytes >= kBulkMinBytes) {
+    // fp64 float + / x / compensated + (fixed-tree partials per bulk chunk): the
+    // vector grid stays ahead up to 1 GiB (2^24-2^26: 3-15% cold, 1-10%
+    // graph-captured; even at 2^27; the ring from 2^28, profiles/
+    // r02_variants_big.json); every other (dtype, op) from 128 MiB
+    const bool f64_blocked = dtype == RD_FLOAT64 && (op == RD_SUM || op == RD_PROD || op == RD_SUM_COMPENSATED);
+    if (bytes >= (f64_blocked ? kBulkMinBytesF64Blocked : kBulkMinBytes)) {
       variant = RD_VARIANT_BULK;      // planner: large inputs take the bulk-copy pipeline
     } else if (bytes > (uint64_t)kBlock * kDefaultUnroll4 * kDefaultVec && bytes <= kClusterMaxBytes &&
                !(cfg && cfg->grid > kClusterMax)) {

@@ -69,6 +69,7 @@ constexpr int kBulkStageBytes = 32768;
 // AUTO picks the bulk pipeline at or above this many input bytes (below it the
 // vector kernel's shorter latency chain wins).
 constexpr uint64_t kBulkMinBytes = 128ull << 20;
+constexpr uint64_t kBulkMinBytesF64Blocked = 1ull << 30;   // fp64 float + / x / compensated + (rd_api.cu)
 // AUTO picks the one-cluster kernel (at most kClusterMax = 16 CTAs, a
 // non-portable cluster size allowed on sm_100) for 32 KB < n*s <= 1 MiB: up to
 // 512 KB the vector plan needs 2..16 CTAs anyway; at 512 KB - 1 MiB 16 CTAs

@@ -320,6 +320,34 @@ def do_exactvariants(args):
     return rows
 
 
+def do_variants(args):
+    """Plain ops at mid sizes (2^20..2^27): vector vs bulk, cold single launch (L2
+    flushed) and graph-captured, for the 8-byte dtypes and a few 4-byte ones -- does
+    the plain planner's 128 MiB bulk threshold (measured on float32 sum) hold?"""
+    rows = []
+    pairs = (("float64", "sum"), ("float64", "max"), ("int64", "sum"), ("float64", "argmax"),
+             ("float32", "argmax"), ("float64", "sum_compensated"))
+    if os.environ.get("SWEEP_PAIRS"):           # e.g. SWEEP_PAIRS=float64:sum,float32:prod
+        pairs = [tuple(p.split(":")) for p in os.environ["SWEEP_PAIRS"].split(",")]
+    for dtype, op in pairs:
+        for log2n in (args.log2n if os.environ.get("SWEEP_PAIRS") else range(20, 28)):
+            n = 1 << log2n
+            x = make(n, dtype, inputs.default_workload(dtype, op))
+            o = torch.empty(2, dtype=torch.int64, device="cuda") if op in rd.ARG_OPS else \
+                torch.empty((), dtype=x.dtype, device="cuda")
+            _, info = rd.reduce_ex(x, op, out=o)
+            for variant in ("vector", "bulk"):
+                fn = lambda: rd.reduce_ex(x, op, variant=variant, out=o)
+                cold = time_launch(fn, n * x.element_size(), reps=20)
+                r = {"dtype": dtype, "op": op, "n": n, "log2n": log2n, "variant": variant,
+                     "auto_variant": info["variant"], "cold_us": round(cold["t_med_us"], 2),
+                     "graph_us": graph_us(fn)}
+                rows.append(r)
+                print(json.dumps(r), flush=True)
+            del x
+    return rows
+
+
 def do_grids(args):
     """Grid multiplier (waves of resident CTAs) for the default kernels at n = 2^28."""
     rows = []
@@ -518,14 +546,14 @@ def do_context(args):
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("what", choices=["probe", "ablation", "ops", "sizes", "grids", "crossover", "multi", "overhead",
-                                    "exact", "midgrids", "midops", "context", "exactvariants"])
+                                    "exact", "midgrids", "midops", "context", "exactvariants", "variants"])
     p.add_argument("--out", required=True)
     p.add_argument("--log2n", type=int, nargs="+", default=[28])
     p.add_argument("--only", nargs="*", default=None, help="ablation: variants to run")
     args = p.parse_args()
     res = {"probe": do_probe, "ablation": do_ablation, "ops": do_ops, "sizes": do_sizes,
            "grids": do_grids, "crossover": do_crossover, "multi": do_multi,
-           "overhead": do_overhead, "exact": do_exact, "exactvariants": do_exactvariants,
+           "overhead": do_overhead, "exact": do_exact, "exactvariants": do_exactvariants, "variants": do_variants,
            "midgrids": do_midgrids, "midops": do_midops, "context": do_context}[args.what](args)
     meta = {"device": torch.cuda.get_device_name(), "what": args.what}
     with open(args.out, "w") as f:
