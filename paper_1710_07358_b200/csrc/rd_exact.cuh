@@ -474,19 +474,23 @@ __device__ __forceinline__ void sacc_flush_warp(long long* w, const double (&d)[
   }
   const bool writer = (int)(threadIdx.x & 31) == __ffs(mask) - 1;
   const long long offset = (long long)__popc(mask) << 38;
+  // value slots no lane of the warp fills (e.g. a1, a2 of fp32 data, which the
+  // group path never touches) are skipped by a warp-uniform branch
+  bool used[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) used[v] = __any_sync(mask, k[v] != kNone);
   int word = __reduce_min_sync(mask, first);
   while (word != kNone) {                            // warp-uniform
     long long c = 0;
     int next = kNone;
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      c += (k[v] == word ? s0[v] : 0) + (k[v] + 1 == word ? s1[v] : 0) + (k[v] + 2 == word ? s2[v] : 0);
+      if (!used[v]) continue;
+      const int r = word - k[v];                     // digit r of value v lands here (r in 0..2)
+      c += r == 0 ? s0[v] : r == 1 ? s1[v] : r == 2 ? s2[v] : 0;
       // this lane's next occupied word above `word` (k, k+1, k+2 of each value)
-      if (k[v] != kNone) {
-        const int d0 = k[v] - word;                  // in [-2, inf)
-        const int cand = d0 > 0 ? k[v] : (d0 > -2 ? k[v] + 2 - (d0 == 0 ? 1 : 0) : kNone);
-        next = min(next, cand);
-      }
+      const int x = word + 1 - k[v];
+      next = min(next, x <= 0 ? k[v] : (x <= 2 ? word + 1 : kNone));
     }
     const unsigned long long u = (unsigned long long)(c + (1ll << 38));   // in [0, 2^39)
     const unsigned c0 = __reduce_add_sync(mask, (unsigned)(u & 0x1fff));
