@@ -673,9 +673,17 @@ __device__ __forceinline__ bool bins_group(WarpBins<K>* wb, uint32_t& flags, con
     const int a0 = top + kBinHead;
     const bool writer = (int)ln == __ffs(mask) - 1;
     const long long off = (long long)__popc(mask) << 50;
+    // (the anchors agree across the lanes by construction -- every re-anchoring
+    // is the warp's -- but a lane left out of a partial-warp call would not
+    // follow one; then each lane deposits its own bins, atomically)
+    const bool uniform = __all_sync(mask, top == __shfl_sync(mask, top, __ffs(mask) - 1));
 #pragma unroll
     for (int j = 0; j < K; ++j) {
       const long long m = __double_as_longlong(wb->s[j][ln]) - __double_as_longlong(bin_anchor(a0 - j * kBinW));
+      if (!uniform) {
+        if (m != 0) sacc_add_units<T>(w, m, a0 - j * kBinW - 52);
+        continue;
+      }
       const unsigned long long u = (unsigned long long)(m + (1ll << 50));          // [0, 2^51)
       const long long tot = (long long)__reduce_add_sync(mask, (unsigned)(u & 0x1ffffu)) +
                             ((long long)__reduce_add_sync(mask, (unsigned)((u >> 17) & 0x1ffffu)) << 17) +
