@@ -47,6 +47,17 @@ def draw_input(rng, dtype, op, n):
     if op == "sum":                          # the float-sum contract is for inputs without overflow
         x = (rng.standard_normal(n) * 10.0 ** rng.integers(-3, 4)).astype(dtype)
         return x, "normal"
+    if op == "sum_exact" and rng.integers(0, 2):
+        # exponents over (a random window of) the whole format: every bin of the exact
+        # sum's binned extraction, re-anchoring, and the per-element levels for fp64
+        lo, hi = (-149, 127) if dtype == "float32" else (-1074, 1023)
+        a = int(rng.integers(lo, hi))
+        b = int(rng.integers(a, hi + 1))
+        e = rng.integers(a, b + 1, n)
+        with np.errstate(over="ignore", under="ignore"):
+            x = (rng.choice([-1.0, 1.0], n) * np.ldexp(rng.random(n) + 0.5, e)).astype(dtype)
+        x[~np.isfinite(x)] = 0
+        return x, "full-range"
     x = (rng.standard_normal(n) * 2.0 ** rng.integers(-60, 60, n)).astype(dtype)
     if n and op != "prod":
         for _ in range(int(rng.integers(0, 4))):
