@@ -52,11 +52,13 @@ rd_status check_dtype_op(int dtype, int op) {
 namespace {
 
 // exact-sum CTA slots: kMaxGrid x (kWords + 1) int64 (the largest, fp64)
-constexpr size_t kExactSlotBytes = sizeof(long long) * kMaxGrid * (ExactTraits<double>::kWords + 1);
+// the exact sum's grid accumulator (kWords + 1 words, zero between launches;
+// rd_exact.cuh exact_finish), one 128-byte-aligned block
+constexpr size_t kExactSlotBytes = (sizeof(long long) * (ExactTraits<double>::kWords + 1) + 127) / 128 * 128;
 
 struct Workspace {
   Slot* partials = nullptr;   // kMaxGrid slots (per CTA, or per chunk for the bulk variant)
-  long long* xpart = nullptr; // exact-sum slots (RD_SUM_EXACT)
+  long long* xpart = nullptr; // exact-sum grid accumulator (RD_SUM_EXACT), zero between launches
   unsigned* ticket = nullptr; // CTAs finished, zero between launches
   unsigned* work = nullptr;   // bulk variant: next chunk, zero between launches
 };

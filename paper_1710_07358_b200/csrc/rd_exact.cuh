@@ -29,9 +29,10 @@
 //  a3-a5  at the end the warp deposits its lanes' expansions cooperatively
 //      (no atomics), carries its words to digits in [0, 2^32), and the CTA
 //      adds its warps' digits.
-//  a6  the CTA's words go to workspace slot blockIdx; the last CTA (atomic
-//      ticket) adds the G slots word by word (integers: any order is exact),
-//      carries (one-cluster form: rank 0 adds the CTAs' words over DSMEM), and
+//  a6  every CTA adds its words into one workspace accumulator with native
+//      64-bit global reductions (integers: any order is exact); the last CTA
+//      (atomic ticket) reads it, zeroes it for the next launch, carries
+//      (one-cluster form: rank 0 adds the CTAs' words over DSMEM), and
 //  a7  rounds once: the 64 bits below the leading one give the p kept bits,
 //      the guard bit and (with every lower digit) the sticky bit; ties to even;
 //      the float is assembled as (shift << (p-1)) + q, which carries a rounded-
@@ -75,7 +76,7 @@ struct XArgs {
   uint64_t n, head, nvec, tail_start, tail;
   void* out;                 // mode 0: one element
   rd_exact_record* rec;      // mode 1: one exact record
-  long long* partials;       // gridDim.x slots of (kWords + 1) words
+  long long* partials;       // the grid accumulator: kWords + 1 words, zero between launches
   unsigned* ticket;
   uint32_t tag;
   int mode;
@@ -1204,38 +1205,33 @@ __device__ __forceinline__ void exact_finish(Ex (&ex)[E], const WarpBins<K>* wbi
                                              long long* tot, unsigned& s_flags, unsigned& s_last,
                                              const XArgs& args) {
   constexpr int NW = ExactTraits<T>::kWords;
-  long long* slot = args.partials + (size_t)blockIdx.x * (NW + 1);
+  static_assert(B > NW, "one thread per word");
+  // a6: the launch's accumulator -- NW + 1 words at the head of the exact
+  // workspace, zero between launches. Every CTA adds its carried words
+  // (< 2^35 each: < 2^47 over any grid) with native 64-bit global reductions
+  // and ORs its flags; integer adds are exact in any order, so the last CTA
+  // (atomic ticket) reads NW + 1 words instead of folding G slots of NW + 1
+  // words (fp64: 296 CTAs x 69 words were ~80 dependent-ish L2 loads per
+  // thread of the last CTA) and zeroes them for the next launch.
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(args.partials);
   exact_cta_words<T, B, E, K>(ex, wbins, flags, sacc, s_flags, tot);
-  if (threadIdx.x <= NW) __stcg(slot + threadIdx.x, tot[threadIdx.x]);
-  // a6: last CTA adds the G slots
+  if (threadIdx.x < NW) {
+    if (tot[threadIdx.x] != 0) atomicAdd(acc + threadIdx.x, (unsigned long long)tot[threadIdx.x]);
+  } else if (threadIdx.x == NW) {
+    if (tot[NW] != 0) atomicOr(acc + NW, (unsigned long long)tot[NW]);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned t = ticket_acq_rel(args.ticket);   // release the CTA's slot words, acquire the others'
+    const unsigned t = ticket_acq_rel(args.ticket);   // release the CTA's additions, acquire the others'
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  const int G = (int)gridDim.x;
-  constexpr int GROUPS = B / (NW + 1);             // (word, slot-group) pairs in parallel
-  if (threadIdx.x < GROUPS * (NW + 1)) {
-    const int j = threadIdx.x % (NW + 1), grp = threadIdx.x / (NW + 1);
-    long long s = 0;
-    for (int g = grp; g < G; g += GROUPS) {
-      const long long v = __ldcg(args.partials + (size_t)g * (NW + 1) + j);
-      s = (j == NW) ? (s | v) : (s + v);           // the flags word is OR-ed
-    }
-    tot[threadIdx.x] = s;
-  }
-  __syncthreads();
   if (threadIdx.x <= NW) {
-    const int j = threadIdx.x;
-    long long s = 0;
-    for (int grp = 0; grp < GROUPS; ++grp) {
-      const long long v = tot[grp * (NW + 1) + j];
-      s = (j == NW) ? (s | v) : (s + v);
-    }
-    if (j < NW) sacc[0][j] = s;
-    else s_flags = (unsigned)s;
+    const long long v = (long long)__ldcg(acc + threadIdx.x);
+    acc[threadIdx.x] = 0ull;                         // zero for the next launch (kernel boundary orders it)
+    if (threadIdx.x < NW) sacc[0][threadIdx.x] = v;
+    else s_flags = (unsigned)v;
   }
   __syncthreads();
   if (threadIdx.x < 32) sacc_normalise_by_warp<NW>(sacc[0]);

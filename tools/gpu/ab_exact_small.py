@@ -5,7 +5,7 @@ L.reduce.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_in
 out = torch.empty(2, dtype=torch.int64, device="cuda")
 res = {}
 DT = int(os.environ.get("AB_DT", "3"))
-for log2n in (14, 16, 18):
+for log2n in [int(v) for v in os.environ.get("AB_LOG2N", "14,16,18").split(",")]:
     x = torch.rand(1 << log2n, device="cuda", dtype=torch.float64 if DT == 4 else torch.float32)
     gs = torch.cuda.Stream()
     with torch.cuda.stream(gs):
