@@ -515,23 +515,26 @@ __device__ __forceinline__ void sacc_flush_warp(long long* w, const double (&d)[
 // nearly every group fails): BINNED EXTRACTION after Demmel & Nguyen's
 // indexed summation (the technique of ReproBLAS), with enough bins and a
 // bounded number of additions that it is EXACT, not only reproducible.
-// Each thread keeps K fp64 bins with fixed exponents a_j = a_0 - j*W (W = 38):
-// bin j holds S_j = 1.5*2^(a_j) + (sum of the pieces it took), and every piece
-// is a multiple of its unit u_j = ulp(S_j) = 2^(a_j - 52). A term x passes
-// down the bins: t = fl(S_j + r); q = t - S_j (exact: Sterbenz); r = r - q
+// Each lane keeps K = 8 fp64 bins with fixed exponents a_j = a_0 - j*W
+// (W = 38; the anchor a_0 is the same in every lane of a warp): bin j holds
+// S_j = 1.5*2^(a_j) + (sum of the pieces it took), and every piece is a
+// multiple of its unit u_j = ulp(S_j) = 2^(a_j - 52). A term x passes down
+// the bins: t = fl(S_j + r); q = t - S_j (exact: Sterbenz); r = r - q
 // (exact: the error of rounding r to a multiple of u_j); S_j = t. Bounds that
 // keep every step exact: |x| <= 2^(a_0 + W - 53) (floor(log2|x|) <= a_0 - 16,
-// else the bins are re-anchored higher) and at most 4096 < 2^(51 - W)
-// additions between re-anchorings, so |S_j - 1.5*2^(a_j)| < 2^(a_j - 2) and
-// S_j never leaves its binade. What falls below the last bin's unit (r != 0
-// after bin K-1) is deposited into the warp's superaccumulator; when every
-// term's lowest bit is at least that unit (checked from the exponent fields,
-// per warp), the last bin is one plain add. Re-anchoring deposits each bin's
-// content S_j - 1.5*2^(a_j) (exact) into the superaccumulator. Per term: 3
-// DADD per bin but the last (1) -- 7 for fp32 (K = 3: 114 + 52 bits below
-// the anchor, the `wide` fp32 range 2^-63..2^41 with 5 bits to spare), 10 for
-// fp64 (K = 4) -- branch-free and independent of the order of the terms
-// (round 1's per-element TwoSum cascade: ~20 dependent FP64 ops per term).
+// else the warp re-anchors higher) and at most 4096 < 2^(51 - W) additions
+// between re-anchorings, so |S_j - 1.5*2^(a_j)| < 2^(a_j - 2) and S_j never
+// leaves its binade. A group runs the fewest bins whose last unit is <= every
+// term's lowest bit (from the exponent fields; per warp: 2, 3, 4 or 8), so
+// nothing falls below the last bin and it is one plain add: 3 DADD per bin
+// but the last (1) -- 7 per term for `wide` fp32 (3 bins), 10 for `wide`
+// fp64 (4), 22 at most -- branch-free and independent of the order of the
+// terms (round 1's per-element TwoSum cascade: ~20 dependent FP64 ops per
+// term). 8 bins span 52 + 7 * 38 = 318 bits: every fp32 exponent; fp64
+// groups that reach past them take the per-element levels. Re-anchoring
+// moves each bin's content (the difference of the bit patterns of S_j and
+// 1.5*2^(a_j), in units of u_j) into the warp's superaccumulator, summed over
+// the warp first.
 constexpr int kBinW = 38;                  // bits per bin
 constexpr int kBinHead = 54 - kBinW;       // bins take floor(log2|x|) <= a_0 - kBinHead
 constexpr int kBinSlack = 4;               // a new anchor leaves this many binades of room above the max
